@@ -1,0 +1,78 @@
+"""Seeded synthetic inputs shared by tests, smoke() and bench.py.
+
+This module holds input generators only -- none of the method's arithmetic.
+Both the CPU oracle (``oracle/``) and the CUDA product path consume what it
+produces; neither imports the other.
+
+Recipe:
+* Taylor-Green lattice (reading Z26): x = lo + (i + 1/2) h, h = L/n, one
+  particle per lattice node, alpha = omega_TG(x) h^3, sigma = overlap * h.
+  The paper's workload is a uniform particle lattice carrying vorticity
+  (P:212 reinitialisation to the same positions; P:243 256^3 per process).
+* Tiled Taylor-Green (reading Z27): P_x x P_y x P_z copies of the 2 pi cube,
+  one copy per GPU for weak scaling (C5).
+* Random clouds: uniform positions (seeds 1106 and 5273 by convention),
+  alpha ~ N(0, 1) h^3, used for stress and brute-force cases.
+All arrays are float32, the boundary's precision.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TWO_PI = 2.0 * np.pi
+
+
+def omega_tg(x):
+    """Vorticity of u_TG = (sin x cos y cos z, -cos x sin y cos z, 0) (Z26)."""
+    x = np.asarray(x, dtype=np.float64)
+    X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+    return np.stack([-np.cos(X) * np.sin(Y) * np.sin(Z),
+                     -np.sin(X) * np.cos(Y) * np.sin(Z),
+                     2.0 * np.sin(X) * np.sin(Y) * np.cos(Z)], axis=-1)
+
+
+def lattice(n: int, lo=-np.pi, L=TWO_PI, tiles=(1, 1, 1)):
+    """Cell-centred lattice of n^3 points per tile; tiles extend along +x,+y,+z.
+
+    Ordering: x fastest, then y, then z, then tile (x-fastest)."""
+    h = L / n
+    c = lo + (np.arange(n, dtype=np.float64) + 0.5) * h
+    Z, Y, X = np.meshgrid(c, c, c, indexing="ij")
+    base = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=-1)
+    out = []
+    for tz in range(tiles[2]):
+        for ty in range(tiles[1]):
+            for tx in range(tiles[0]):
+                out.append(base + np.array([tx * L, ty * L, tz * L]))
+    return np.concatenate(out, axis=0), h
+
+
+def taylor_green(n: int, overlap: float = 1.0, lo=-np.pi, L=TWO_PI, tiles=(1, 1, 1)):
+    """Taylor-Green vortex particles on an n^3 lattice per tile.
+
+    Returns (x, alpha, sigma) float32 arrays of shapes [N,3], [N,3], [N]."""
+    x, h = lattice(n, lo, L, tiles)
+    alpha = omega_tg(x) * h ** 3
+    sigma = np.full(x.shape[0], overlap * h)
+    return (x.astype(np.float32), alpha.astype(np.float32), sigma.astype(np.float32))
+
+
+def random_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI, sigma=None, h=None):
+    """Uniform random positions in [lo, lo+L)^3 with alpha ~ N(0,1) h^3."""
+    rng = np.random.default_rng(seed)
+    x = lo + L * rng.random((n, 3))
+    if h is None:
+        h = L / max(1.0, round(n ** (1.0 / 3.0)))
+    alpha = rng.standard_normal((n, 3)) * h ** 3
+    sig = np.full(n, h if sigma is None else sigma)
+    return x.astype(np.float32), alpha.astype(np.float32), sig.astype(np.float32)
+
+
+def jittered_lattice(n: int, seed: int = 5273, lo=-np.pi, L=TWO_PI, overlap=1.0):
+    """Taylor-Green lattice with positions jittered by +-h/4 (key boundaries)."""
+    x, a, s = taylor_green(n, overlap, lo, L)
+    h = L / n
+    rng = np.random.default_rng(seed)
+    xj = x.astype(np.float64) + (rng.random(x.shape) - 0.5) * 0.5 * h
+    xj = np.clip(xj, lo, np.nextafter(np.float32(lo + L), np.float32(lo)))
+    return xj.astype(np.float32), a, s
