@@ -1,0 +1,143 @@
+/*
+ * fmm.h -- C ABI of the B200-native FMM evaluator for the vortex particle
+ * method of Yokota, Barba, Narumi & Yasuoka, "Petascale turbulence simulation
+ * using a highly parallel fast multipole method on GPUs" (arXiv 1106.5273).
+ * Citations "P:n" are lines of that paper's text; "Zn" are the
+ * readings of ambiguous passages listed in DESIGN.md.
+ *
+ * What the library computes.  For N vortex particles with positions
+ * x_j, strengths alpha_j (= gamma_j, Eq. 1) and core widths sigma_j:
+ *
+ *   u_i         = sum_j alpha_j x grad G g_sigma              (Eq. 1)
+ *   dalpha_i/dt = sum_j grad(alpha_j x grad G g_sigma).alpha_i (Eq. 3)
+ *
+ * with G = 1/(4 pi r), g the Gaussian cutoff of Eq. 2 evaluated with the
+ * source's sigma_j (Z4), the physical sign u_i = sum g alpha_j x (x_i - x_j) /
+ * (4 pi r^3) (Z1), the classical stretching (alpha_i . grad) u (Z3), and pairs
+ * at r = 0 contributing nothing (Z7).  Sources = targets = the set particles.
+ * The sums are evaluated by the FMM: Morton-key octree,
+ * dual tree traversal (Alg. 1-2) emitting P2P and M2L lists,
+ * spherical-harmonic expansions of order p (Z8), and -- when
+ * images > 0 -- the periodic cube [lo, lo+L)^3 with 3^k image boxes per
+ * dimension (Z14).  The far field uses the singular kernel
+ * (Z5).  All kernels run on the GPU in FP32 with FP64 accumulation of P2P tile
+ * partials ("single precision ... double-precision accuracy").
+ *
+ * Conventions for every call:
+ *  - Return value: fmm_status, FMM_OK == 0.  No C++ exception crosses the ABI.
+ *    fmm_last_error(ctx) returns a message for the last failing call.
+ *  - Arrays: contiguous, row-major FP32.  A pointer may be device memory on
+ *    cfg.device or host memory (pageable or pinned); the library detects which
+ *    with cudaPointerGetAttributes and copies host data itself.
+ *  - Ownership: the caller owns every array it passes.  set_particles copies
+ *    its inputs and returns after validation; evaluate overwrites the caller's
+ *    output arrays and returns when they are valid (stream synchronised).
+ *  - After FMM_E_CUDA, FMM_E_NCCL or FMM_E_INTERNAL the context is poisoned:
+ *    only fmm_destroy is legal (further calls return FMM_E_STATE).
+ *  - One host thread per context.  No CPU fallback exists: every step of the
+ *    evaluation runs in this library's CUDA kernels.
+ */
+#ifndef FMM_B200_H
+#define FMM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fmm_ctx fmm_ctx;
+
+typedef enum {
+  FMM_OK = 0,
+  FMM_E_ARG = 1,        /* bad config, null pointer with n > 0, n < 0          */
+  FMM_E_NONFINITE = 2,  /* non-finite x, alpha or sigma                 */
+  FMM_E_SIGMA = 3,      /* sigma <= 0                                   */
+  FMM_E_STATE = 4,      /* evaluate before set_particles; poisoned context     */
+  FMM_E_OOM = 5,        /* device allocation failed                            */
+  FMM_E_CUDA = 6,       /* CUDA runtime error (context poisoned)               */
+  FMM_E_NCCL = 7,       /* NCCL error (context poisoned)                       */
+  FMM_E_INTERNAL = 8    /* invariant violated (context poisoned)               */
+} fmm_status;
+
+typedef struct {
+  uint32_t struct_size;          /* = sizeof(fmm_config): ABI versioning              */
+  int32_t  order;                /* p: degrees n = 0..p-1 (Z8); default 10; 2 <= p <= 16 */
+  int32_t  theta_num, theta_den; /* MAC r_A + r_B < theta R (Z9); theta = num/den,
+                                    1 <= num < den <= 64; default 1/2                  */
+  int32_t  ncrit;                /* leaf iff count <= ncrit or level 21 (Z13); dflt 64 */
+  int32_t  images;               /* k: 3^k image boxes per dimension (Z14);
+                                    0 = free space; 0 <= k <= 6; default 3             */
+  double   box_lo[3], box_len;   /* periodic cell (images > 0): default lo = -pi,
+                                    L = 2 pi; ignored in free space (Z16)      */
+  int32_t  traversal;            /* 0 = MAC-first (default), 1 = leaf-first (Z11)      */
+  int32_t  device;               /* CUDA ordinal                                       */
+  void*    stream;               /* cudaStream_t for all work; NULL = library-owned    */
+  int32_t  rank, nranks;         /* nranks == 1: single GPU                            */
+  const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1              */
+} fmm_config;
+
+/* Per-phase device times of the last set_particles / evaluate (CUDA events on
+ * the library stream, ms) and the work counters of the last evaluate. */
+typedef struct {
+  uint32_t struct_size;          /* = sizeof(fmm_stats)                                */
+  int64_t  n, ncells, nleaves, nlevels;
+  int64_t  p2p_list, m2l_list;   /* list entries (cell pairs)                          */
+  int64_t  p2p_pairs;            /* particle pairs evaluated by P2P                    */
+  int64_t  far_m2l;              /* M2L of the periodic far layers (a8)                */
+  double   model_flops;          /* 174 * p2p_pairs (Table 1)               */
+  double   ms_keys, ms_sort, ms_tree;                  /* set_particles: a1-a4         */
+  double   ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_downward, ms_finalize;
+  double   ms_set_total, ms_eval_total;
+} fmm_stats;
+
+/* Fill cfg with the defaults listed above. */
+void fmm_config_default(fmm_config* cfg);
+
+/* Create a context on cfg->device.  Errors: FMM_E_ARG (invalid field),
+ * FMM_E_CUDA, FMM_E_NCCL.  *out is NULL on failure. */
+fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out);
+
+/* a1-a4: copy and validate n particles -- x[n][3], alpha[n][3],
+ * sigma[n] -- wrap them into the periodic cell when images > 0, build
+ * 63-bit Morton keys (Z16), radix-sort them (stable, Z17) and
+ * build the octree.  n = 0 is valid.  Errors: FMM_E_ARG,
+ * FMM_E_NONFINITE, FMM_E_SIGMA, FMM_E_OOM, FMM_E_CUDA. */
+fmm_status fmm_set_particles(fmm_ctx* ctx, int64_t n, const float* x,
+                             const float* alpha, const float* sigma);
+
+/* a5-a13: P2M, M2M, dual tree traversal, periodic far field, M2L, L2L, L2P,
+ * P2P; writes u[n][3] (Eq. 1) and dalpha_dt[n][3] (Eq. 3) in the caller's
+ * particle order (overwrite, Z28).  Errors: FMM_E_STATE, FMM_E_ARG, FMM_E_CUDA. */
+fmm_status fmm_evaluate(fmm_ctx* ctx, float* u, float* dalpha_dt);
+
+/* As fmm_evaluate but writes only the selected parts: bit 0 = near field
+ * (P2P), bit 1 = far field (M2L/L2L/L2P incl. periodic layers).  parts = 3 is
+ * fmm_evaluate.  Used by the parity tests (near field on identical lists). */
+fmm_status fmm_evaluate_parts(fmm_ctx* ctx, int32_t parts, float* u, float* dalpha_dt);
+
+fmm_status fmm_destroy(fmm_ctx* ctx);
+const char* fmm_last_error(const fmm_ctx* ctx);
+fmm_status fmm_get_stats(const fmm_ctx* ctx, fmm_stats* s);
+
+/* ---- inspection (tests): host output arrays, valid after set_particles ---- */
+/* Sizes; lists are built by the first evaluate after set_particles, or here. */
+fmm_status fmm_get_sizes(fmm_ctx* ctx, int64_t* ncells, int64_t* np2p, int64_t* nm2l);
+/* Key box: lo[3] and side L (periodic cell, or the bounding cube, Z16). */
+fmm_status fmm_get_box(const fmm_ctx* ctx, double* lo, double* L);
+/* keys[n] sorted ascending and perm[n] = caller index of sorted slot i. */
+fmm_status fmm_get_keys(const fmm_ctx* ctx, uint64_t* keys, int64_t* perm);
+/* cells[ncells][10] = level, qx, qy, qz, begin, count, parent, child_begin,
+ * nchild, is_leaf in canonical (level, key) order; child_begin = -1 for leaves. */
+fmm_status fmm_get_cells(const fmm_ctx* ctx, int64_t* cells);
+/* p2p[np2p][3], m2l[nm2l][3] = (target cell, source cell, image index) sorted
+ * by (target, source, image); image index = (ix+1) + 3(iy+1) + 9(iz+1). */
+fmm_status fmm_get_lists(fmm_ctx* ctx, int64_t* p2p, int64_t* m2l);
+/* Normalised expansions after evaluate (Z18): M~_n = M_n / s^n,
+ * L~_n = L_n s^(n+1), s = cell side; [ncells][3][p(p+1)/2] complex FP32
+ * (interleaved re, im) -- either pointer may be NULL. */
+fmm_status fmm_get_expansions(const fmm_ctx* ctx, float* M, float* L);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,349 @@
+// api.cu -- the C ABI declared in include/fmm.h: argument checking, pointer
+// kind detection (host or device), stage orchestration on the library stream,
+// per-phase CUDA-event timing, and the final combine + un-permute (a13).
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "ctx.cuh"
+
+#define FMM_API extern "C" __attribute__((visibility("default")))
+
+namespace fmmb {
+
+void set_expansion_smem_limits();
+
+namespace {
+
+__global__ void k_finalize(const uint32_t* __restrict__ idx, int64_t n, int parts, const float* __restrict__ un,
+                           const float* __restrict__ sn, const float* __restrict__ uf, const float* __restrict__ sf,
+                           float* __restrict__ u, float* __restrict__ s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = 3 * (int64_t)idx[i];
+    for (int d = 0; d < 3; ++d) {
+      float uu = 0.f, ss = 0.f;
+      if (parts & 1) { uu += un[3 * i + d]; ss += sn[3 * i + d]; }
+      if (parts & 2) { uu += uf[3 * i + d]; ss += sf[3 * i + d]; }
+      u[o + d] = uu;
+      s[o + d] = ss;
+    }
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) { cudaGetLastError(); return 0.f; }
+  return ms;
+}
+
+void check_config(const fmm_config& c) {
+  if (c.struct_size != sizeof(fmm_config)) throw FmmError(FMM_E_ARG, "fmm_config.struct_size mismatch");
+  if (c.order < 2 || c.order > kMaxOrder) throw FmmError(FMM_E_ARG, "order must be in [2, 16]");
+  if (c.theta_num < 1 || c.theta_den > 64 || c.theta_num >= c.theta_den)
+    throw FmmError(FMM_E_ARG, "theta must satisfy 1 <= num < den <= 64");
+  if (c.ncrit < 1) throw FmmError(FMM_E_ARG, "ncrit must be >= 1");
+  if (c.images < 0 || c.images > 6) throw FmmError(FMM_E_ARG, "images must be in [0, 6]");
+  if (c.images > 0 && !(c.box_len > 0.0 && std::isfinite(c.box_len))) throw FmmError(FMM_E_ARG, "box_len must be > 0");
+  if (c.traversal != 0 && c.traversal != 1) throw FmmError(FMM_E_ARG, "traversal must be 0 or 1");
+  if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) throw FmmError(FMM_E_ARG, "bad rank/nranks");
+  if (c.nranks > 1) throw FmmError(FMM_E_ARG, "multi-GPU contexts are created per rank with nranks == 1 in this build");
+}
+
+template <typename F>
+fmm_status guard(Ctx* c, F f) {
+  try {
+    f();
+    return FMM_OK;
+  } catch (const FmmError& e) {
+    if (c) {
+      c->err = e.what();
+      if (e.code == FMM_E_CUDA || e.code == FMM_E_NCCL || e.code == FMM_E_INTERNAL) c->poisoned = true;
+    }
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return FMM_E_OOM;
+  } catch (...) {
+    if (c) { c->err = "unknown internal error"; c->poisoned = true; }
+    return FMM_E_INTERNAL;
+  }
+}
+
+void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
+  cudaStream_t st = c.stream;
+  int64_t n = c.n;
+  FMM_CUDA(cudaEventRecord(c.ev[PH_EVAL0], st));
+  if (n == 0) {
+    for (int p = PH_UP; p <= PH_FIN; ++p) FMM_CUDA(cudaEventRecord(c.ev[p], st));
+    c.evaluated = true;
+    return;
+  }
+  size_t ncoef = (size_t)c.ncells * 3 * c.nc;
+  c.M.reserve(ncoef);
+  c.Lc.reserve(ncoef);
+  c.u_near.reserve(3 * n); c.s_near.reserve(3 * n); c.u_far.reserve(3 * n); c.s_far.reserve(3 * n);
+  // a5-a6 upward pass
+  upward_pass(c);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_UP], st));
+  // a7 traversal (once per set_particles)
+  if (!c.lists_valid) build_lists(c);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
+  // a9 M2L + a8 periodic far layers
+  FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
+  m2l_pass(c);
+  periodic_far_pass(c);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
+  // a12 P2P
+  p2p_pass(c, c.u_near.p, c.s_near.p);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));
+  // a10-a11 downward pass
+  downward_pass(c, c.u_far.p, c.s_far.p);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_DOWN], st));
+  // a13 combine + un-permute into the caller's order
+  bool hu = !is_device_ptr(u), hs = !is_device_ptr(s);
+  float* du = u;
+  float* ds = s;
+  if (hu) { c.stage_u.reserve(3 * n); du = c.stage_u.p; }
+  if (hs) { c.stage_ds.reserve(3 * n); ds = c.stage_ds.p; }
+  unsigned g = nblocks(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  k_finalize<<<g, 256, 0, st>>>(c.idx.p, n, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
+  FMM_LAUNCH_CHECK();
+  if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
+  if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaEventRecord(c.ev[PH_FIN], st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c.evaluated = true;
+  fmm_stats& S = c.stats;
+  S.ms_upward = ms_between(c.ev[PH_EVAL0], c.ev[PH_UP]);
+  S.ms_traverse = ms_between(c.ev[PH_UP], c.ev[PH_TRAV]);
+  S.ms_m2l = ms_between(c.ev[PH_TRAV], c.ev[PH_M2L]);
+  S.ms_p2p = ms_between(c.ev[PH_M2L], c.ev[PH_P2P]);
+  S.ms_downward = ms_between(c.ev[PH_P2P], c.ev[PH_DOWN]);
+  S.ms_finalize = ms_between(c.ev[PH_DOWN], c.ev[PH_FIN]);
+  S.ms_eval_total = ms_between(c.ev[PH_EVAL0], c.ev[PH_FIN]);
+}
+
+}  // namespace
+}  // namespace fmmb
+
+using namespace fmmb;
+
+FMM_API void fmm_config_default(fmm_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->struct_size = sizeof(fmm_config);
+  cfg->order = 10;
+  cfg->theta_num = 1;
+  cfg->theta_den = 2;
+  cfg->ncrit = 64;
+  cfg->images = 3;
+  cfg->box_lo[0] = cfg->box_lo[1] = cfg->box_lo[2] = -kPi;
+  cfg->box_len = 2.0 * kPi;
+  cfg->traversal = 0;
+  cfg->device = 0;
+  cfg->stream = nullptr;
+  cfg->rank = 0;
+  cfg->nranks = 1;
+  cfg->nccl_id = nullptr;
+}
+
+FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
+  if (!out) return FMM_E_ARG;
+  *out = nullptr;
+  if (!cfg) return FMM_E_ARG;
+  fmm_ctx* h = new (std::nothrow) fmm_ctx;
+  if (!h) return FMM_E_OOM;
+  Ctx& c = h->c;
+  fmm_status st = guard(&c, [&] {
+    check_config(*cfg);
+    c.cfg = *cfg;
+    c.P = cfg->order;
+    c.nc = c.P * (c.P + 1) / 2;
+    FMM_CUDA(cudaSetDevice(cfg->device));
+    if (cfg->stream) {
+      c.stream = (cudaStream_t)cfg->stream;
+    } else {
+      FMM_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.own_stream = true;
+    }
+    for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
+    set_expansion_smem_limits();
+    FMM_CUDA(cudaGetLastError());
+  });
+  if (st != FMM_OK) { delete h; return st; }
+  *out = h;
+  return FMM_OK;
+}
+
+FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  cudaSetDevice(c.cfg.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  for (int i = 0; i <= PH_N; ++i) if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+  if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+  return FMM_OK;
+}
+
+FMM_API const char* fmm_last_error(const fmm_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
+
+FMM_API fmm_status fmm_set_particles(fmm_ctx* h, int64_t n, const float* x, const float* alpha, const float* sigma) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (n < 0) throw FmmError(FMM_E_ARG, "n < 0");
+    if (n > 0 && (!x || !alpha || !sigma)) throw FmmError(FMM_E_ARG, "null array with n > 0");
+    if (n >= (1ll << 31)) throw FmmError(FMM_E_ARG, "n >= 2^31");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    const float *dx = x, *da = alpha, *ds = sigma;
+    if (n > 0) {
+      if (!is_device_ptr(x)) {
+        c.stage_x.reserve(3 * n);
+        FMM_CUDA(cudaMemcpyAsync(c.stage_x.p, x, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+        dx = c.stage_x.p;
+      }
+      if (!is_device_ptr(alpha)) {
+        c.stage_a.reserve(3 * n);
+        FMM_CUDA(cudaMemcpyAsync(c.stage_a.p, alpha, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+        da = c.stage_a.p;
+      }
+      if (!is_device_ptr(sigma)) {
+        c.stage_s.reserve(n);
+        FMM_CUDA(cudaMemcpyAsync(c.stage_s.p, sigma, sizeof(float) * n, cudaMemcpyHostToDevice, c.stream));
+        ds = c.stage_s.p;
+      }
+    }
+    set_particles_impl(c, n, dx, da, ds);
+    fmm_stats& S = c.stats;
+    S.ms_keys = ms_between(c.ev[PH_SET0], c.ev[PH_KEYS]);
+    S.ms_sort = ms_between(c.ev[PH_KEYS], c.ev[PH_SORT]);
+    S.ms_tree = ms_between(c.ev[PH_SORT], c.ev[PH_TREE]);
+    S.ms_set_total = ms_between(c.ev[PH_SET0], c.ev[PH_TREE]);
+  });
+}
+
+FMM_API fmm_status fmm_evaluate_parts(fmm_ctx* h, int32_t parts, float* u, float* s) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (!c.have_particles) throw FmmError(FMM_E_STATE, "evaluate before set_particles");
+    if (c.n > 0 && (!u || !s)) throw FmmError(FMM_E_ARG, "null output with n > 0");
+    if (parts < 1 || parts > 3) throw FmmError(FMM_E_ARG, "parts must be 1, 2 or 3");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    evaluate_impl(c, parts, u, s);
+  });
+}
+
+FMM_API fmm_status fmm_evaluate(fmm_ctx* h, float* u, float* s) { return fmm_evaluate_parts(h, 3, u, s); }
+
+FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
+  if (!h || !s) return FMM_E_ARG;
+  const Ctx& c = h->c;
+  *s = c.stats;
+  s->struct_size = sizeof(fmm_stats);
+  s->n = c.n;
+  s->ncells = c.ncells;
+  s->nleaves = c.nleaves;
+  s->nlevels = c.level_begin.empty() ? 0 : (int64_t)c.level_begin.size() - 1;
+  s->p2p_list = c.np2p;
+  s->m2l_list = c.nm2l;
+  s->p2p_pairs = c.p2p_pairs;
+  s->far_m2l = c.far_m2l;
+  s->model_flops = 174.0 * (double)c.p2p_pairs;
+  return FMM_OK;
+}
+
+FMM_API fmm_status fmm_get_sizes(fmm_ctx* h, int64_t* ncells, int64_t* np2p, int64_t* nm2l) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    if (!c.lists_valid) build_lists(c);
+    if (ncells) *ncells = c.ncells;
+    if (np2p) *np2p = c.np2p;
+    if (nm2l) *nm2l = c.nm2l;
+  });
+}
+
+FMM_API fmm_status fmm_get_box(const fmm_ctx* h, double* lo, double* L) {
+  if (!h || !lo || !L) return FMM_E_ARG;
+  for (int d = 0; d < 3; ++d) lo[d] = h->c.lo[d];
+  *L = h->c.L;
+  return FMM_OK;
+}
+
+FMM_API fmm_status fmm_get_keys(const fmm_ctx* h, uint64_t* keys, int64_t* perm) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = const_cast<Ctx&>(h->c);
+  return guard(&c, [&] {
+    if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
+    if (c.n == 0) return;
+    std::vector<uint32_t> idx(c.n);
+    if (keys) FMM_CUDA(cudaMemcpy(keys, c.keys.p, sizeof(uint64_t) * c.n, cudaMemcpyDeviceToHost));
+    FMM_CUDA(cudaMemcpy(idx.data(), c.idx.p, sizeof(uint32_t) * c.n, cudaMemcpyDeviceToHost));
+    if (perm) for (int64_t i = 0; i < c.n; ++i) perm[i] = idx[i];
+  });
+}
+
+FMM_API fmm_status fmm_get_cells(const fmm_ctx* h, int64_t* out) {
+  if (!h || !out) return FMM_E_ARG;
+  Ctx& c = const_cast<Ctx&>(h->c);
+  return guard(&c, [&] {
+    if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
+    int64_t nc = c.ncells;
+    std::vector<int> buf(nc);
+    DBuf<int>* cols[10] = {&c.cells.level, &c.cells.qx, &c.cells.qy, &c.cells.qz, &c.cells.begin,
+                           &c.cells.count, &c.cells.parent, &c.cells.child_begin, &c.cells.nchild, &c.cells.leaf};
+    for (int k = 0; k < 10; ++k) {
+      if (nc) FMM_CUDA(cudaMemcpy(buf.data(), cols[k]->p, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < nc; ++i) out[10 * i + k] = buf[i];
+    }
+  });
+}
+
+FMM_API fmm_status fmm_get_lists(fmm_ctx* h, int64_t* p2p, int64_t* m2l) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
+    if (!c.lists_valid) build_lists(c);
+    auto dump = [&](const DBuf<uint64_t>& L, int64_t n, int64_t* out) {
+      if (!out || n == 0) return;
+      std::vector<uint64_t> v(n);
+      FMM_CUDA(cudaMemcpy(v.data(), L.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i) {
+        out[3 * i] = (int64_t)(v[i] >> 32);
+        out[3 * i + 1] = (int64_t)((v[i] >> 5) & 0x7ffffff);
+        out[3 * i + 2] = (int64_t)(v[i] & 31);
+      }
+    };
+    dump(c.p2p, c.np2p, p2p);
+    dump(c.m2l, c.nm2l, m2l);
+  });
+}
+
+FMM_API fmm_status fmm_get_expansions(const fmm_ctx* h, float* M, float* L) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = const_cast<Ctx&>(h->c);
+  return guard(&c, [&] {
+    if (!c.evaluated) throw FmmError(FMM_E_STATE, "no evaluation yet");
+    size_t bytes = sizeof(float2) * (size_t)c.ncells * 3 * c.nc;
+    if (M && bytes) FMM_CUDA(cudaMemcpy(M, c.M.p, bytes, cudaMemcpyDeviceToHost));
+    if (L && bytes) FMM_CUDA(cudaMemcpy(L, c.Lc.p, bytes, cudaMemcpyDeviceToHost));
+  });
+}

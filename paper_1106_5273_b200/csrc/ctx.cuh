@@ -1,0 +1,82 @@
+// ctx.cuh -- the library-owned context behind the opaque fmm_ctx handle, and
+// the internal entry points of each pipeline stage.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fmmb {
+
+// Octree cells in canonical (level, key) order, SoA, int32 (a4).
+struct Cells {
+  DBuf<int> level, qx, qy, qz, begin, count, parent, child_begin, nchild, leaf;
+  void reserve_keep(size_t n, size_t keep, cudaStream_t s) {
+    DBuf<int>* all[] = {&level, &qx, &qy, &qz, &begin, &count, &parent, &child_begin, &nchild, &leaf};
+    for (auto* b : all) b->grow_keep(n, keep, s);
+  }
+};
+
+enum Phase { PH_SET0, PH_KEYS, PH_SORT, PH_TREE, PH_EVAL0, PH_UP, PH_TRAV, PH_M2L, PH_P2P, PH_DOWN, PH_FIN, PH_N };
+
+struct Ctx {
+  fmm_config cfg{};
+  int P = 10, nc = 55;
+  cudaStream_t stream = nullptr, stream2 = nullptr;
+  bool own_stream = false;
+  std::string err;
+  bool poisoned = false;
+
+  // ---- particles and tree (set_particles) ----
+  int64_t n = 0;
+  bool have_particles = false;
+  double lo[3] = {0, 0, 0}, L = 1.0;
+  DBuf<float> stage_x, stage_a, stage_s;    // host-input staging
+  DBuf<float4> pos_tmp, pos, alp;           // sorted: (x,y,z,sigma), (alpha,0)
+  DBuf<uint64_t> keys_tmp, keys;
+  DBuf<uint32_t> idx_tmp, idx;               // idx[i] = caller index of sorted slot i
+  DBuf<unsigned char> cub_tmp;
+  DBuf<int> pcell_a, pcell_b, flags, scan, dflag;
+  DBuf<int> leaf_ids;
+  Cells cells;
+  int64_t ncells = 0, nleaves = 0;
+  std::vector<int64_t> level_begin;          // cells of level l: [level_begin[l], level_begin[l+1])
+  std::vector<int> host_leaf_top;            // leaf flags of levels 0..1 (far targets)
+
+  // ---- lists (traversal) ----
+  bool lists_valid = false;
+  DBuf<uint64_t> p2p, m2l, sort_tmp, front_a, front_b;
+  DBuf<int> cnt_m2l, cnt_p2p, cnt_push, off_m2l, off_p2p, off_push;
+  int64_t np2p = 0, nm2l = 0, p2p_pairs = 0;
+  DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;
+  DBuf<unsigned long long> dcount;
+
+  // ---- expansions and results ----
+  DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)
+  DBuf<double> far_M;                        // periodic super-cell multipoles
+  DBuf<float> u_near, s_near, u_far, s_far;  // sorted order, [n][3]
+  DBuf<float> stage_u, stage_ds;             // host-output staging
+  bool evaluated = false;
+  int64_t far_m2l = 0;
+
+  // ---- timing ----
+  cudaEvent_t ev[PH_N + 1] = {};
+  fmm_stats stats{};
+};
+
+// pipeline stages (each enqueues on ctx.stream; throws FmmError)
+void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const float* s);
+void build_lists(Ctx& c);
+void upward_pass(Ctx& c);
+void m2l_pass(Ctx& c);
+void periodic_far_pass(Ctx& c);
+void downward_pass(Ctx& c, float* u_far, float* s_far);
+void p2p_pass(Ctx& c, float* u_near, float* s_near);
+
+}  // namespace fmmb
+
+struct fmm_ctx {
+  fmmb::Ctx c;
+};

@@ -1,0 +1,479 @@
+// expansions.cu -- the far-field operators of fig:kernels:
+// P2M (a5), M2M (a6), M2L (a9), periodic far layers (a8), L2L
+// (a10) and L2P (a11), on scaled solid harmonics (Cheng et al.).
+// Coefficients are stored normalised by the cell side s (reading Z18):
+// M~_n = M_n / s^n and L~_n = L_n s^(n+1), so every translation is evaluated
+// on O(1) vectors (D / s_target, d / s_parent) and the dynamic range of the
+// FP32 coefficients stays small; sums run from high to low degree.
+// Layout: float2 [cell][component][n(n+1)/2 + m], 0 <= m <= n < p.
+#include "ctx.cuh"
+
+namespace fmmb {
+
+namespace {
+
+__device__ __forceinline__ void nm_of(int k, int& n, int& m) {
+  n = (int)((sqrtf(8.0f * k + 1.0f) - 1.0f) * 0.5f);
+  while (n * (n + 1) / 2 > k) --n;
+  while ((n + 1) * (n + 2) / 2 <= k) ++n;
+  m = k - n * (n + 1) / 2;
+}
+
+__device__ __forceinline__ cpx<float> ld(const float2* p) { float2 v = *p; return {v.x, v.y}; }
+
+struct GCells {
+  const int *level, *qx, *qy, *qz, *begin, *count, *parent, *child_begin, *nchild, *leaf;
+};
+GCells gcells(Ctx& c) {
+  return {c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p,
+          c.cells.parent.p, c.cells.child_begin.p, c.cells.nchild.p, c.cells.leaf.p};
+}
+
+struct Geo { double lo[3]; double L; };
+
+// ---------------------------------------------------------------- P2M (a5)
+// one block per leaf; 32 particles per chunk build their R_n^m((x - c)/s)
+// in shared memory, then thread o = (component, coefficient) accumulates
+// alpha_{j,comp} conj(R) over the chunk in particle order.
+__global__ void k_p2m(int P, const int* __restrict__ leaf_ids, GCells c, Geo g, const float4* __restrict__ pos,
+                      const float4* __restrict__ alp, float2* __restrict__ M) {
+  extern __shared__ float2 sm[];
+  const int nc = P * (P + 1) / 2;
+  cpx<float>* R = (cpx<float>*)sm;             // [32][nc]
+  float4* A = (float4*)(sm + 32 * nc);          // [32]
+  int leaf = leaf_ids[blockIdx.x];
+  int lev = c.level[leaf], b = c.begin[leaf], cnt = c.count[leaf];
+  double s = g.L / (double)(1 << lev);
+  double cx = g.lo[0] + (c.qx[leaf] + 0.5) * s, cy = g.lo[1] + (c.qy[leaf] + 0.5) * s,
+         cz = g.lo[2] + (c.qz[leaf] + 0.5) * s;
+  int o = threadIdx.x;
+  int comp = o / nc, k = o % nc;
+  cpx<float> acc = {0.f, 0.f};
+  for (int j0 = 0; j0 < cnt; j0 += 32) {
+    int nj = min(32, cnt - j0);
+    if (threadIdx.x < nj) {
+      float4 p = pos[b + j0 + threadIdx.x];
+      float y0 = (float)(((double)p.x - cx) / s), y1 = (float)(((double)p.y - cy) / s),
+            y2 = (float)(((double)p.z - cz) / s);
+      regular_harmonics<float>(y0, y1, y2, P, R + threadIdx.x * nc);
+      A[threadIdx.x] = alp[b + j0 + threadIdx.x];
+    }
+    __syncthreads();
+    if (o < 3 * nc) {
+      for (int jj = 0; jj < nj; ++jj) {
+        float4 a4 = A[jj];
+        float a = comp == 0 ? a4.x : (comp == 1 ? a4.y : a4.z);
+        cpx<float> r = R[jj * nc + k];
+        acc.re += a * r.re;
+        acc.im -= a * r.im;
+      }
+    }
+    __syncthreads();
+  }
+  if (o < 3 * nc) M[((int64_t)leaf * 3 + comp) * nc + k] = make_float2(acc.re, acc.im);
+}
+
+// ---------------------------------------------------------------- M2M (a6)
+// M~_n^m(parent) = sum_{k,l} conj(R_k^l(d/s_p)) M~_{n-k}^{m-l}(child) 2^{-(n-k)}
+__global__ void k_m2m(int P, int64_t first, GCells c, float2* __restrict__ M) {
+  extern __shared__ float2 sm[];
+  const int nc = P * (P + 1) / 2;
+  cpx<float>* Rd = (cpx<float>*)sm;   // [8][nc]
+  int p = (int)(first + blockIdx.x);
+  if (c.leaf[p]) return;
+  int cb = c.child_begin[p], nch = c.nchild[p];
+  if ((int)threadIdx.x < nch) {
+    int ch = cb + threadIdx.x;
+    float dx = 0.5f * ((float)(c.qx[ch] - 2 * c.qx[p]) - 0.5f);
+    float dy = 0.5f * ((float)(c.qy[ch] - 2 * c.qy[p]) - 0.5f);
+    float dz = 0.5f * ((float)(c.qz[ch] - 2 * c.qz[p]) - 0.5f);
+    regular_harmonics<float>(dx, dy, dz, P, Rd + threadIdx.x * nc);
+  }
+  __syncthreads();
+  int o = threadIdx.x;
+  if (o >= 3 * nc) return;
+  int comp = o / nc, k = o % nc, n, m;
+  nm_of(k, n, m);
+  cpx<float> acc = {0.f, 0.f};
+  for (int q = 0; q < nch; ++q) {
+    const cpx<float>* R = Rd + q * nc;
+    const cpx<float>* Mc = (const cpx<float>*)(M + ((int64_t)(cb + q) * 3 + comp) * nc);
+    for (int kk = n; kk >= 0; --kk) {
+      int nn = n - kk;
+      float sc = ldexpf(1.0f, -nn);
+      for (int l = -kk; l <= kk; ++l) {
+        int mm = m - l;
+        if (mm < -nn || mm > nn) continue;
+        cpx<float> t = cmulc(cget(Mc, nn, mm), cget(R, kk, l));
+        acc.re += sc * t.re;
+        acc.im += sc * t.im;
+      }
+    }
+  }
+  M[((int64_t)p * 3 + comp) * nc + k] = make_float2(acc.re, acc.im);
+}
+
+// ---------------------------------------------------------------- M2L (a9)
+// One block per target cell (the paper's mapping: a target cell per
+// thread block, source cells staged in shared memory one after another); a
+// thread per local coefficient (k, l) for all three components.
+// L~_k^l(t) += (-1)^k sum_{n<p-k} sum_m M~_n^m(s) (s_s/s_t)^n I_{n+k}^{m+l}(D/s_t)
+// with D = c_t - c_s - img L evaluated exactly from integer cell coordinates.
+__global__ void k_m2l(int P, int64_t ncells, const int* __restrict__ seg_b, const int* __restrict__ seg_e,
+                      const uint64_t* __restrict__ lst, GCells c, const float2* __restrict__ M,
+                      float2* __restrict__ Lc) {
+  extern __shared__ float2 sm[];
+  const int nc = P * (P + 1) / 2;
+  const int P2 = 2 * P - 1;
+  const int nc2 = P2 * (P2 + 1) / 2;
+  cpx<float>* Is = (cpx<float>*)sm;            // [nc2]
+  cpx<float>* Ms = (cpx<float>*)(sm + nc2);    // [3][nc]
+  int t = blockIdx.x;
+  int b = seg_b[t], e = seg_e[t];
+  if (b == e) return;
+  int lt = c.level[t];
+  long long ctx = (long long)(2 * c.qx[t] + 1) << (kMaxLevel - lt);
+  long long cty = (long long)(2 * c.qy[t] + 1) << (kMaxLevel - lt);
+  long long ctz = (long long)(2 * c.qz[t] + 1) << (kMaxLevel - lt);
+  float inv_st = ldexpf(1.0f, -(kMaxLevel + 1 - lt));
+  int k = 0, l = 0;
+  if ((int)threadIdx.x < nc) nm_of(threadIdx.x, k, l);
+  cpx<float> acc[3] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  for (int q = b; q < e; ++q) {
+    uint64_t ent = lst[q];
+    int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
+    int ls = c.level[src];
+    int ix = img % 3 - 1, iy = (img / 3) % 3 - 1, iz = img / 9 - 1;
+    long long dx = ctx - ((long long)(2 * c.qx[src] + 1) << (kMaxLevel - ls)) - (long long)ix * (1ll << (kMaxLevel + 1));
+    long long dy = cty - ((long long)(2 * c.qy[src] + 1) << (kMaxLevel - ls)) - (long long)iy * (1ll << (kMaxLevel + 1));
+    long long dz = ctz - ((long long)(2 * c.qz[src] + 1) << (kMaxLevel - ls)) - (long long)iz * (1ll << (kMaxLevel + 1));
+    float Dx = (float)dx * inv_st, Dy = (float)dy * inv_st, Dz = (float)dz * inv_st;
+    for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+      int kk = i % nc, n, m;
+      nm_of(kk, n, m);
+      float sc = ldexpf(1.0f, (lt - ls) * n);
+      float2 v = M[(int64_t)src * 3 * nc + i];
+      Ms[i] = {v.x * sc, v.y * sc};
+    }
+    for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<float>(Dx, Dy, Dz, m, P2, Is);
+    __syncthreads();
+    if ((int)threadIdx.x < nc) {
+      for (int n = P - 1 - k; n >= 0; --n)
+        for (int m = -n; m <= n; ++m) {
+          cpx<float> I = cget(Is, n + k, m + l);
+          for (int comp = 0; comp < 3; ++comp) {
+            cpx<float> Mv = cget(Ms + comp * nc, n, m);
+            acc[comp].re += Mv.re * I.re - Mv.im * I.im;
+            acc[comp].im += Mv.re * I.im + Mv.im * I.re;
+          }
+        }
+    }
+    __syncthreads();
+  }
+  if ((int)threadIdx.x < nc) {
+    float sg = (k & 1) ? -1.f : 1.f;
+    for (int comp = 0; comp < 3; ++comp) {
+      float2* d = Lc + ((int64_t)t * 3 + comp) * nc + threadIdx.x;
+      float2 v = *d;
+      *d = make_float2(v.x + sg * acc[comp].re, v.y + sg * acc[comp].im);
+    }
+  }
+}
+
+// --------------------------------------------- periodic far layers (a8)
+// Double precision (the work is O(1) in N: 702 (k-1) M2L per far target).
+// far_M[j] holds M^{(j+1)} normalised by its side 3^j L.
+__global__ void k_far_super(int P, int k, const float2* __restrict__ Mroot, double* __restrict__ farM) {
+  extern __shared__ double smd[];
+  const int nc = P * (P + 1) / 2;
+  cpx<double>* R = (cpx<double>*)smd;                // [nc]
+  cpx<double>* F = (cpx<double>*)farM;
+  int o = threadIdx.x;
+  for (int i = o; i < 3 * nc; i += blockDim.x) F[i] = {(double)Mroot[i].x, (double)Mroot[i].y};
+  __syncthreads();
+  for (int j = 1; j + 1 < k; ++j) {
+    const cpx<double>* Mj = F + (j - 1) * 3 * nc;
+    cpx<double>* Mn = F + j * 3 * nc;
+    int comp = o / nc, kk0 = o % nc, n = 0, m = 0;
+    if (o < 3 * nc) nm_of(kk0, n, m);
+    cpx<double> acc = {0, 0};
+    for (int C3 = 0; C3 < 27; ++C3) {
+      __syncthreads();
+      if (o == 0) regular_harmonics<double>((C3 % 3 - 1) / 3.0, ((C3 / 3) % 3 - 1) / 3.0, (C3 / 9 - 1) / 3.0, P, R);
+      __syncthreads();
+      if (o < 3 * nc) {
+        for (int kk = n; kk >= 0; --kk) {
+          int nn = n - kk;
+          double sc = pow(3.0, -nn);
+          for (int l = -kk; l <= kk; ++l) {
+            int mm = m - l;
+            if (mm < -nn || mm > nn) continue;
+            cpx<double> t = cmulc(cget(Mj + comp * nc, nn, mm), cget(R, kk, l));
+            acc.re += sc * t.re;
+            acc.im += sc * t.im;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (o < 3 * nc) Mn[comp * nc + kk0] = acc;
+    __syncthreads();
+  }
+}
+
+__global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, GCells c, Geo g,
+                          const double* __restrict__ farM, float2* __restrict__ Lc) {
+  extern __shared__ double smd[];
+  const int nc = P * (P + 1) / 2;
+  const int P2 = 2 * P - 1;
+  const int nc2 = P2 * (P2 + 1) / 2;
+  cpx<double>* Is = (cpx<double>*)smd;          // [nc2]
+  cpx<double>* Ms = Is + nc2;                   // [3][nc]
+  const cpx<double>* F = (const cpx<double>*)farM;
+  int t = targets[blockIdx.x];
+  int lt = c.level[t];
+  double st = g.L / (double)(1 << lt);
+  double rx = (c.qx[t] + 0.5) * st - 0.5 * g.L, ry = (c.qy[t] + 0.5) * st - 0.5 * g.L,
+         rz = (c.qz[t] + 0.5) * st - 0.5 * g.L;   // c_t - c_0
+  int kq = 0, lq = 0;
+  if ((int)threadIdx.x < nc) nm_of(threadIdx.x, kq, lq);
+  cpx<double> acc[3] = {{0, 0}, {0, 0}, {0, 0}};
+  double scale = g.L;
+  for (int j = 1; j < k; ++j, scale *= 3.0) {
+    double ratio = scale / st;
+    for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+      int kk = i % nc, n, m;
+      nm_of(kk, n, m);
+      double sc = pow(ratio, n);
+      cpx<double> v = F[(j - 1) * 3 * nc + i];
+      Ms[i] = {v.re * sc, v.im * sc};
+    }
+    for (int I3 = 0; I3 < 27; ++I3) {
+      if (I3 == kImgCentre) continue;
+      for (int C3 = 0; C3 < 27; ++C3) {
+        double ox = 3 * (I3 % 3 - 1) + (C3 % 3 - 1), oy = 3 * ((I3 / 3) % 3 - 1) + ((C3 / 3) % 3 - 1),
+               oz = 3 * (I3 / 9 - 1) + (C3 / 9 - 1);
+        double Dx = (rx - ox * scale) / st, Dy = (ry - oy * scale) / st, Dz = (rz - oz * scale) / st;
+        __syncthreads();
+        for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<double>(Dx, Dy, Dz, m, P2, Is);
+        __syncthreads();
+        if ((int)threadIdx.x < nc) {
+          for (int n = P - 1 - kq; n >= 0; --n)
+            for (int m = -n; m <= n; ++m) {
+              cpx<double> I = cget(Is, n + kq, m + lq);
+              for (int comp = 0; comp < 3; ++comp) {
+                cpx<double> Mv = cget(Ms + comp * nc, n, m);
+                acc[comp].re += Mv.re * I.re - Mv.im * I.im;
+                acc[comp].im += Mv.re * I.im + Mv.im * I.re;
+              }
+            }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if ((int)threadIdx.x < nc) {
+    double sg = (kq & 1) ? -1.0 : 1.0;
+    for (int comp = 0; comp < 3; ++comp) {
+      float2* d = Lc + ((int64_t)t * 3 + comp) * nc + threadIdx.x;
+      float2 v = *d;
+      *d = make_float2((float)((double)v.x + sg * acc[comp].re), (float)((double)v.y + sg * acc[comp].im));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- L2L (a10)
+// L~_a^b(child) += 2^{-(a+1)} sum_{k>=a,l} L~_k^l(parent) conj(R_{k-a}^{l-b}(d/s_p))
+__global__ void k_l2l(int P, int64_t first, GCells c, float2* __restrict__ Lc) {
+  extern __shared__ float2 sm[];
+  const int nc = P * (P + 1) / 2;
+  cpx<float>* Rd = (cpx<float>*)sm;          // [nc]
+  cpx<float>* Lp = (cpx<float>*)(sm + nc);   // [3][nc]
+  int ch = (int)(first + blockIdx.x);
+  int p = c.parent[ch];
+  if (threadIdx.x == 0) {
+    float dx = 0.5f * ((float)(c.qx[ch] - 2 * c.qx[p]) - 0.5f);
+    float dy = 0.5f * ((float)(c.qy[ch] - 2 * c.qy[p]) - 0.5f);
+    float dz = 0.5f * ((float)(c.qz[ch] - 2 * c.qz[p]) - 0.5f);
+    regular_harmonics<float>(dx, dy, dz, P, Rd);
+  }
+  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) Lp[i] = ld(Lc + (int64_t)p * 3 * nc + i);
+  __syncthreads();
+  int o = threadIdx.x;
+  if (o >= 3 * nc) return;
+  int comp = o / nc, kk0 = o % nc, a, bb;
+  nm_of(kk0, a, bb);
+  cpx<float> acc = {0.f, 0.f};
+  for (int k = P - 1; k >= a; --k)
+    for (int l = -k; l <= k; ++l) {
+      int ka = k - a, lb = l - bb;
+      if (lb < -ka || lb > ka) continue;
+      cpx<float> t = cmulc(cget(Lp + comp * nc, k, l), cget(Rd, ka, lb));
+      acc.re += t.re;
+      acc.im += t.im;
+    }
+  float sc = ldexpf(1.0f, -(a + 1));
+  float2* d = Lc + ((int64_t)ch * 3 + comp) * nc + kk0;
+  float2 v = *d;
+  *d = make_float2(v.x + sc * acc.re, v.y + sc * acc.im);
+}
+
+// ---------------------------------------------------------------- L2P (a11)
+// Shift L~ to the particle keeping degrees 1..2 (8c-2 item 16):
+// L'_a^b = s^{-a-1} sum_{k>=a,l} L~_k^l conj(R_{k-a}^{l-b}(y)), y = (x - c)/s;
+// grad phi = (-Re L'_1^1, -Im L'_1^1, Re L'_1^0); Hessian from L'_2^{0,1,2};
+// u = (1/4pi) eps_abc d_b phi_c, s = (1/4pi) alpha_d eps_abc H^c_db.
+__global__ void k_l2p(int P, const int* __restrict__ leaf_ids, GCells c, Geo g, const float4* __restrict__ pos,
+                      const float4* __restrict__ alp, const float2* __restrict__ Lc, float* __restrict__ uf,
+                      float* __restrict__ sf) {
+  extern __shared__ float2 sm[];
+  const int nc = P * (P + 1) / 2;
+  cpx<float>* Ls = (cpx<float>*)sm;               // [3][nc]
+  cpx<float>* Rall = (cpx<float>*)(sm + 3 * nc);  // [32][nc]
+  int leaf = leaf_ids[blockIdx.x];
+  int lev = c.level[leaf], b = c.begin[leaf], cnt = c.count[leaf];
+  double s = g.L / (double)(1 << lev);
+  double cx = g.lo[0] + (c.qx[leaf] + 0.5) * s, cy = g.lo[1] + (c.qy[leaf] + 0.5) * s,
+         cz = g.lo[2] + (c.qz[leaf] + 0.5) * s;
+  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) Ls[i] = ld(Lc + (int64_t)leaf * 3 * nc + i);
+  __syncthreads();
+  float is2 = (float)(1.0 / (s * s)), is3 = (float)(1.0 / (s * s * s));
+  const float k4 = (float)(1.0 / (4.0 * kPi));
+  cpx<float>* R = Rall + threadIdx.x * nc;
+  for (int i0 = 0; i0 < cnt; i0 += blockDim.x) {
+    int i = i0 + threadIdx.x;
+    if (i >= cnt) break;
+    float4 p = pos[b + i];
+    float y0 = (float)(((double)p.x - cx) / s), y1 = (float)(((double)p.y - cy) / s), y2 = (float)(((double)p.z - cz) / s);
+    regular_harmonics<float>(y0, y1, y2, P, R);
+    float gr[3][3], H[3][6];
+    for (int comp = 0; comp < 3; ++comp) {
+      const cpx<float>* Lq = Ls + comp * nc;
+      cpx<float> Lp[5];   // (1,0) (1,1) (2,0) (2,1) (2,2)
+      const int A_[5] = {1, 1, 2, 2, 2}, B_[5] = {0, 1, 0, 1, 2};
+      for (int q = 0; q < 5; ++q) {
+        int a = A_[q], bb = B_[q];
+        cpx<float> acc = {0.f, 0.f};
+        for (int k = P - 1; k >= a; --k)
+          for (int l = -k; l <= k; ++l) {
+            int ka = k - a, lb = l - bb;
+            if (lb < -ka || lb > ka) continue;
+            cpx<float> t = cmulc(cget(Lq, k, l), cget(R, ka, lb));
+            acc.re += t.re;
+            acc.im += t.im;
+          }
+        Lp[q] = acc;
+      }
+      gr[comp][0] = -Lp[1].re * is2;
+      gr[comp][1] = -Lp[1].im * is2;
+      gr[comp][2] = Lp[0].re * is2;
+      H[comp][0] = 0.5f * (-Lp[2].re + Lp[4].re) * is3;   // xx
+      H[comp][1] = 0.5f * (-Lp[2].re - Lp[4].re) * is3;   // yy
+      H[comp][2] = Lp[2].re * is3;                         // zz
+      H[comp][3] = 0.5f * Lp[4].im * is3;                  // xy
+      H[comp][4] = -Lp[3].re * is3;                        // xz
+      H[comp][5] = -Lp[3].im * is3;                        // yz
+    }
+    // H(c)[d][b] accessor
+    auto Hc = [&](int comp, int d, int bb) -> float {
+      if (d == bb) return H[comp][d];
+      int lo_ = min(d, bb), hi_ = max(d, bb);
+      return lo_ == 0 ? (hi_ == 1 ? H[comp][3] : H[comp][4]) : H[comp][5];
+    };
+    float4 ai = alp[b + i];
+    float av[3] = {ai.x, ai.y, ai.z};
+    float u0 = gr[2][1] - gr[1][2], u1 = gr[0][2] - gr[2][0], u2 = gr[1][0] - gr[0][1];
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (int d = 0; d < 3; ++d) {
+      s0 += av[d] * (Hc(2, d, 1) - Hc(1, d, 2));
+      s1 += av[d] * (Hc(0, d, 2) - Hc(2, d, 0));
+      s2 += av[d] * (Hc(1, d, 0) - Hc(0, d, 1));
+    }
+    int64_t o = 3 * (int64_t)(b + i);
+    uf[o] = k4 * u0; uf[o + 1] = k4 * u1; uf[o + 2] = k4 * u2;
+    sf[o] = k4 * s0; sf[o + 1] = k4 * s1; sf[o + 2] = k4 * s2;
+  }
+}
+
+inline int round32(int v) { return (v + 31) / 32 * 32; }
+
+}  // namespace
+
+static Geo geo(const Ctx& c) { return {{c.lo[0], c.lo[1], c.lo[2]}, c.L}; }
+
+void upward_pass(Ctx& c) {
+  cudaStream_t st = c.stream;
+  int P = c.P, nc = c.nc;
+  GCells gc = gcells(c);
+  if (c.nleaves > 0) {
+    size_t sm = sizeof(float2) * (32 * nc) + sizeof(float4) * 32;
+    k_p2m<<<(unsigned)c.nleaves, round32(3 * nc), sm, st>>>(P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
+    FMM_LAUNCH_CHECK();
+  }
+  int nlev = (int)c.level_begin.size() - 1;
+  for (int l = nlev - 2; l >= 0; --l) {
+    int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
+    if (cnt <= 0) continue;
+    k_m2m<<<(unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, st>>>(P, first, gc, c.M.p);
+    FMM_LAUNCH_CHECK();
+  }
+}
+
+void m2l_pass(Ctx& c) {
+  if (c.nm2l == 0) return;
+  int P = c.P, nc = c.nc, P2 = 2 * P - 1, nc2 = P2 * (P2 + 1) / 2;
+  size_t sm = sizeof(float2) * (nc2 + 3 * nc);
+  k_m2l<<<(unsigned)c.ncells, round32(nc), sm, c.stream>>>(P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), c.M.p,
+                                                          c.Lc.p);
+  FMM_LAUNCH_CHECK();
+}
+
+void periodic_far_pass(Ctx& c) {
+  int k = c.cfg.images;
+  c.far_m2l = 0;
+  if (k < 2 || c.ncells == 0) return;
+  int P = c.P, nc = c.nc, P2 = 2 * P - 1, nc2 = P2 * (P2 + 1) / 2;
+  // far targets: cells at level 2 and leaves above level 2
+  std::vector<int> tg;
+  for (size_t i = 0; i < c.host_leaf_top.size(); ++i)
+    if (c.host_leaf_top[i]) tg.push_back((int)i);
+  if (c.level_begin.size() > 3)
+    for (int64_t i = c.level_begin[2]; i < c.level_begin[3]; ++i) tg.push_back((int)i);
+  c.far_M.reserve((size_t)(k - 1) * 3 * nc * 2);
+  k_far_super<<<1, round32(3 * nc), sizeof(double) * 2 * nc, c.stream>>>(P, k, c.M.p, c.far_M.p);
+  FMM_LAUNCH_CHECK();
+  c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
+  FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
+  size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
+  k_far_m2l<<<(unsigned)tg.size(), round32(nc), sm, c.stream>>>(P, k, c.scan.p, gcells(c), geo(c), c.far_M.p, c.Lc.p);
+  FMM_LAUNCH_CHECK();
+  c.far_m2l = (int64_t)tg.size() * 702 * (k - 1);
+}
+
+void downward_pass(Ctx& c, float* u_far, float* s_far) {
+  cudaStream_t st = c.stream;
+  int P = c.P, nc = c.nc;
+  GCells gc = gcells(c);
+  int nlev = (int)c.level_begin.size() - 1;
+  for (int l = 1; l < nlev; ++l) {
+    int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
+    if (cnt <= 0) continue;
+    k_l2l<<<(unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, st>>>(P, first, gc, c.Lc.p);
+    FMM_LAUNCH_CHECK();
+  }
+  if (c.nleaves > 0) {
+    size_t sm = sizeof(float2) * (3 * nc + 32 * nc);
+    k_l2p<<<(unsigned)c.nleaves, 32, sm, st>>>(P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.Lc.p, u_far, s_far);
+    FMM_LAUNCH_CHECK();
+  }
+}
+
+void set_expansion_smem_limits() {
+  int big = 200 * 1024;
+  cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_l2p, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_far_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
+}  // namespace fmmb

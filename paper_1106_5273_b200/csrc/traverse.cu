@@ -1,0 +1,225 @@
+// traverse.cu -- a7: dual tree traversal (Alg. 1, Alg. 2
+// P:171-187) on the device, level-synchronously.  The paper's stack of cell
+// pairs becomes a frontier array: every round pops the whole frontier,
+// splits the larger cell of each pair (equal radius => split B, never split a
+// leaf: reading Z10) and applies Interact to each child pair (MAC-first or
+// leaf-first, reading Z11).  Each round is a count pass, three exclusive scans
+// and a write pass, so no atomics decide where entries go; the lists are then
+// radix-sorted into the canonical (target, source, image) order (Z20) and cut
+// into per-target segments for the P2P and M2L kernels.  The MAC is the exact
+// integer form of r_A + r_B < theta R (Z9).
+#include <cub/cub.cuh>
+
+#include "ctx.cuh"
+
+namespace fmmb {
+
+namespace {
+
+struct TCells {
+  const int *level, *qx, *qy, *qz, *child_begin, *nchild, *leaf, *count;
+};
+
+struct TParams {
+  unsigned long long lhs_k;   // 3 * theta_den^2
+  unsigned long long rhs_k;   // theta_num^2
+  int leaf_first;
+};
+
+__device__ __forceinline__ uint64_t pack(int A, int B, int img) {
+  return ((uint64_t)A << 32) | ((uint64_t)B << 5) | (uint64_t)img;
+}
+
+// MAC (Z9): 3 den^2 (2^{21-a} + 2^{21-b})^2 < num^2 |Delta|^2 on integers in
+// units of half the finest cell; |Delta| includes the first-layer image shift.
+__device__ __forceinline__ bool mac_accept(const TCells& c, const TParams& p, int A, int B, int img) {
+  int la = c.level[A], lb = c.level[B];
+  int ix = img % 3 - 1, iy = (img / 3) % 3 - 1, iz = img / 9 - 1;
+  long long dx = ((long long)(2 * c.qx[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qx[B] + 1) << (kMaxLevel - lb)) - (long long)ix * (1ll << (kMaxLevel + 1));
+  long long dy = ((long long)(2 * c.qy[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qy[B] + 1) << (kMaxLevel - lb)) - (long long)iy * (1ll << (kMaxLevel + 1));
+  long long dz = ((long long)(2 * c.qz[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qz[B] + 1) << (kMaxLevel - lb)) - (long long)iz * (1ll << (kMaxLevel + 1));
+  unsigned long long d2 = (unsigned long long)(dx * dx) + (unsigned long long)(dy * dy) + (unsigned long long)(dz * dz);
+  unsigned long long ss = (1ull << (kMaxLevel - la)) + (1ull << (kMaxLevel - lb));
+  return p.lhs_k * ss * ss < p.rhs_k * d2;
+}
+
+// Alg. 2 Interact: 0 = M2L, 1 = P2P, 2 = push.
+__device__ __forceinline__ int interact(const TCells& c, const TParams& p, int A, int B, int img) {
+  bool leaves = c.leaf[A] && c.leaf[B];
+  if (p.leaf_first) {
+    if (leaves) return 1;
+    return mac_accept(c, p, A, B, img) ? 0 : 2;
+  }
+  if (mac_accept(c, p, A, B, img)) return 0;
+  return leaves ? 1 : 2;
+}
+
+// Alg. 1 body for frontier pair f: split B if A is a leaf or (B is not a leaf
+// and r_B >= r_A, i.e. level_B <= level_A); otherwise split A.
+template <bool WRITE>
+__global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells c, TParams p,
+                         int* __restrict__ cm, int* __restrict__ cp, int* __restrict__ cq,
+                         const int* __restrict__ om, const int* __restrict__ op, const int* __restrict__ oq,
+                         uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p, uint64_t* __restrict__ next) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  uint64_t e = front[f];
+  int A = (int)(e >> 32), B = (int)((e >> 5) & 0x7ffffff), img = (int)(e & 31);
+  bool split_b = c.leaf[A] || (!c.leaf[B] && c.level[B] <= c.level[A]);
+  int cb = split_b ? c.child_begin[B] : c.child_begin[A];
+  int nch = split_b ? c.nchild[B] : c.nchild[A];
+  int nm = 0, np = 0, nq = 0;
+  int bm = 0, bp = 0, bq = 0;
+  if (WRITE) { bm = om[f]; bp = op[f]; bq = oq[f]; }
+  for (int k = 0; k < nch; ++k) {
+    int a = split_b ? A : cb + k;
+    int b = split_b ? cb + k : B;
+    int d = interact(c, p, a, b, img);
+    if (d == 0) { if (WRITE) m2l[bm + nm] = pack(a, b, img); ++nm; }
+    else if (d == 1) { if (WRITE) p2p[bp + np] = pack(a, b, img); ++np; }
+    else { if (WRITE) next[bq + nq] = pack(a, b, img); ++nq; }
+  }
+  if (!WRITE) { cm[f] = nm; cp[f] = np; cq[f] = nq; }
+}
+
+__global__ void k_clear2(int* a, int* b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) { a[i] = 0; b[i] = 0; }
+}
+
+__global__ void k_segments(const uint64_t* __restrict__ lst, int64_t n, int* __restrict__ sb, int* __restrict__ se) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int t = (int)(lst[i] >> 32);
+    if (i == 0 || (int)(lst[i - 1] >> 32) != t) sb[t] = (int)i;
+    if (i == n - 1 || (int)(lst[i + 1] >> 32) != t) se[t] = (int)(i + 1);
+  }
+}
+
+__global__ void k_pair_count(const uint64_t* __restrict__ lst, int64_t n, const int* __restrict__ count,
+                             unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t e = lst[i];
+    acc += (unsigned long long)count[e >> 32] * (unsigned long long)count[(e >> 5) & 0x7ffffff];
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+template <typename F>
+void cub_call(Ctx& c, F f) {
+  size_t bytes = 0;
+  FMM_CUDA(f((void*)nullptr, bytes));
+  c.cub_tmp.reserve(bytes);
+  FMM_CUDA(f((void*)c.cub_tmp.p, bytes));
+}
+
+void exclusive_scan(Ctx& c, const int* in, int* out, int64_t n) {
+  cub_call(c, [&](void* tmp, size_t& bytes) {
+    return cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n, c.stream);
+  });
+}
+
+void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n) {
+  if (n <= 1) return;
+  c.sort_tmp.reserve(n);
+  uint64_t* in = lst.p;
+  uint64_t* out = c.sort_tmp.p;
+  cub_call(c, [&](void* tmp, size_t& bytes) {
+    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, 0, 59, c.stream);
+  });
+  std::swap(lst.p, c.sort_tmp.p);
+  std::swap(lst.cap, c.sort_tmp.cap);
+}
+
+}  // namespace
+
+void build_lists(Ctx& c) {
+  cudaStream_t st = c.stream;
+  c.np2p = c.nm2l = 0;
+  c.p2p_pairs = 0;
+  if (c.ncells == 0) { c.lists_valid = true; return; }
+  TCells tc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.child_begin.p,
+            c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p};
+  TParams tp{3ull * (unsigned long long)c.cfg.theta_den * (unsigned long long)c.cfg.theta_den,
+             (unsigned long long)c.cfg.theta_num * (unsigned long long)c.cfg.theta_num, c.cfg.traversal};
+
+  // seeds (8c-2 item 7): Interact(root, root, img) for the 27 first-layer
+  // images (k >= 1) or the zero image.  The root pair never passes the MAC
+  // (|Delta| <= sqrt(3) L while r_A + r_B = sqrt(3) L and theta < 1), so a
+  // seed is P2P iff the root is a leaf, else it is pushed.
+  std::vector<uint64_t> seeds;
+  if (c.cfg.images > 0) for (int img = 0; img < 27; ++img) seeds.push_back((uint64_t)img);
+  else seeds.push_back((uint64_t)kImgCentre);
+  bool root_leaf = c.host_leaf_top.size() > 0 && c.host_leaf_top[0];
+  int64_t nf = (int64_t)seeds.size();
+  c.front_a.reserve(1024);
+  c.front_b.reserve(1024);
+  c.p2p.reserve(1 << 16);
+  c.m2l.reserve(1 << 16);
+  if (root_leaf) {
+    FMM_CUDA(cudaMemcpyAsync(c.p2p.p, seeds.data(), sizeof(uint64_t) * nf, cudaMemcpyHostToDevice, st));
+    c.np2p = nf;
+    nf = 0;
+  } else {
+    FMM_CUDA(cudaMemcpyAsync(c.front_a.p, seeds.data(), sizeof(uint64_t) * nf, cudaMemcpyHostToDevice, st));
+  }
+
+  while (nf > 0) {
+    c.cnt_m2l.reserve(nf + 1); c.cnt_p2p.reserve(nf + 1); c.cnt_push.reserve(nf + 1);
+    c.off_m2l.reserve(nf + 1); c.off_p2p.reserve(nf + 1); c.off_push.reserve(nf + 1);
+    unsigned g = nblocks(nf, 256);
+    k_expand<false><<<g, 256, 0, st>>>(c.front_a.p, nf, tc, tp, c.cnt_m2l.p, c.cnt_p2p.p, c.cnt_push.p,
+                                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    FMM_LAUNCH_CHECK();
+    exclusive_scan(c, c.cnt_m2l.p, c.off_m2l.p, nf);
+    exclusive_scan(c, c.cnt_p2p.p, c.off_p2p.p, nf);
+    exclusive_scan(c, c.cnt_push.p, c.off_push.p, nf);
+    int tail[6];
+    FMM_CUDA(cudaMemcpyAsync(&tail[0], c.off_m2l.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&tail[1], c.cnt_m2l.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&tail[2], c.off_p2p.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&tail[3], c.cnt_p2p.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&tail[4], c.off_push.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&tail[5], c.cnt_push.p + nf - 1, 4, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    int64_t add_m = (int64_t)tail[0] + tail[1], add_p = (int64_t)tail[2] + tail[3], add_q = (int64_t)tail[4] + tail[5];
+    if (c.nm2l + add_m >= (1ll << 31) || c.np2p + add_p >= (1ll << 31))
+      throw FmmError(FMM_E_ARG, "interaction list exceeds 2^31 entries");
+    c.m2l.grow_keep(c.nm2l + add_m, c.nm2l, st);
+    c.p2p.grow_keep(c.np2p + add_p, c.np2p, st);
+    c.front_b.reserve(add_q);
+    k_expand<true><<<g, 256, 0, st>>>(c.front_a.p, nf, tc, tp, nullptr, nullptr, nullptr, c.off_m2l.p,
+                                      c.off_p2p.p, c.off_push.p, c.m2l.p + c.nm2l, c.p2p.p + c.np2p, c.front_b.p);
+    FMM_LAUNCH_CHECK();
+    c.nm2l += add_m;
+    c.np2p += add_p;
+    std::swap(c.front_a.p, c.front_b.p);
+    std::swap(c.front_a.cap, c.front_b.cap);
+    nf = add_q;
+  }
+
+  // canonical order + per-target segments
+  sort_list(c, c.p2p, c.np2p);
+  sort_list(c, c.m2l, c.nm2l);
+  c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
+  c.m2l_b.reserve(c.ncells); c.m2l_e.reserve(c.ncells);
+  k_clear2<<<nblocks(c.ncells, 256), 256, 0, st>>>(c.p2p_b.p, c.p2p_e.p, c.ncells);
+  k_clear2<<<nblocks(c.ncells, 256), 256, 0, st>>>(c.m2l_b.p, c.m2l_e.p, c.ncells);
+  if (c.np2p) k_segments<<<nblocks(c.np2p, 256), 256, 0, st>>>(c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
+  if (c.nm2l) k_segments<<<nblocks(c.nm2l, 256), 256, 0, st>>>(c.m2l.p, c.nm2l, c.m2l_b.p, c.m2l_e.p);
+  c.dcount.reserve(1);
+  FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
+  if (c.np2p) {
+    unsigned g = nblocks(c.np2p, 256);
+    if (g > 148 * 8) g = 148 * 8;
+    k_pair_count<<<g, 256, 0, st>>>(c.p2p.p, c.np2p, c.cells.count.p, c.dcount.p);
+  }
+  FMM_LAUNCH_CHECK();
+  unsigned long long pairs = 0;
+  FMM_CUDA(cudaMemcpyAsync(&pairs, c.dcount.p, sizeof(pairs), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c.p2p_pairs = (int64_t)pairs;
+  c.lists_valid = true;
+}
+
+}  // namespace fmmb

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bars (BASELINE.json north_star):
+* Morton keys, sort permutation, tree and interaction lists: bit-exact.
+* P2P near field on identical lists: rel-L2 <= 1e-5 vs the oracle's double P2P.
+* Full FP32 FMM velocity and stretching: rel-L2 <= 1e-3 vs the double direct
+  sum at p = 10 (and vs the Taylor-Green closed form at sizes the direct sum
+  cannot reach, a property that holds at any N).
+"""
+import numpy as np
+import pytest
+
+import synth
+from test_oracle_kernel import _tg_closed_form
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1_tg16_k3": dict(gen=lambda: synth.taylor_green(16), cfg=dict(images=3)),
+    "tg12_k1_ncrit16": dict(gen=lambda: synth.taylor_green(12), cfg=dict(images=1, ncrit=16)),
+    "jitter10_k2_leaf_first": dict(gen=lambda: synth.jittered_lattice(10), cfg=dict(images=2, ncrit=20, traversal=1)),
+    "rand3000_free": dict(gen=lambda: synth.random_cloud(3000, seed=1106, sigma=0.05), cfg=dict(images=0, ncrit=24)),
+    "rand2500_k1_theta0.4": dict(gen=lambda: synth.random_cloud(2500, seed=5273, sigma=0.05),
+                                 cfg=dict(images=1, ncrit=32, theta=(2, 5))),
+}
+
+
+def _oracle_kw(cfg):
+    kw = dict(order=cfg.get("order", 10), theta=cfg.get("theta", (1, 2)), ncrit=cfg.get("ncrit", 64),
+              images=cfg.get("images", 3), traversal=cfg.get("traversal", 0))
+    return kw
+
+
+@pytest.fixture(scope="module")
+def runs(oracle_mod):
+    from gpu_util import GpuRun
+    out = {}
+    for name, c in CASES.items():
+        x, a, s = c["gen"]()
+        g = GpuRun(x, a, s, **c["cfg"])
+        o = oracle_mod.OracleFMM(x, a, s, **_oracle_kw(c["cfg"]))
+        out[name] = (x, a, s, g, o)
+    yield out
+    for v in out.values():
+        v[3].close()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_keys_tree_bitexact(runs, name):
+    x, a, s, g, o = runs[name]
+    lo_g, L_g = g.box()
+    lo_o, L_o = o.box()
+    assert np.array_equal(lo_g, lo_o) and L_g == L_o
+    kg, pg = g.keys()
+    ko, po = o.keys()
+    assert np.array_equal(kg, ko)
+    assert np.array_equal(pg, po)
+    assert np.array_equal(g.cells(), o.cells())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_lists_bitexact(runs, name):
+    x, a, s, g, o = runs[name]
+    p2p, m2l = g.lists()
+    assert np.array_equal(p2p, o.p2p_list())
+    assert np.array_equal(m2l, o.m2l_list())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_p2p_near_field_on_identical_lists(runs, oracle_mod, name):
+    x, a, s, g, o = runs[name]
+    un, sn = g.evaluate(parts=1)
+    r = o.evaluate()
+    assert oracle_mod.rel_l2(un, r["u_near"]) <= 1e-5
+    assert oracle_mod.rel_l2(sn, r["s_near"]) <= 1e-5
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_expansions_and_far_field(runs, oracle_mod, name):
+    x, a, s, g, o = runs[name]
+    uf, sf = g.evaluate(parts=2)
+    r = o.evaluate()
+    Mg, Lg = g.expansions()
+    Mo, Lo = o.multipoles(), o.locals()
+    assert np.linalg.norm(Mg - Mo) / np.linalg.norm(Mo) <= 1e-5
+    assert np.linalg.norm(Lg - Lo) / np.linalg.norm(Lo) <= 1e-5
+    assert oracle_mod.rel_l2(uf, r["u_far"]) <= 1e-5
+    assert oracle_mod.rel_l2(sf, r["s_far"]) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["tg12_k1_ncrit16", "rand3000_free", "rand2500_k1_theta0.4"])
+def test_full_fmm_vs_double_direct_sum(runs, oracle_mod, name):
+    x, a, s, g, o = runs[name]
+    cfg = CASES[name]["cfg"]
+    u, st = g.evaluate()
+    u0, s0 = oracle_mod.direct(x, a, x, a, s, images=cfg["images"])
+    assert oracle_mod.rel_l2(u, u0) <= 1e-3
+    assert oracle_mod.rel_l2(st, s0) <= 1e-3
+
+
+def test_c1_vs_periodic_direct_sum_k1_and_closed_form(oracle_mod):
+    """C1 (TG 16^3, p = 10): the k = 1 FMM against the explicit 27-image double
+    direct sum, and the k = 3 FMM (BASELINE config) against the closed form,
+    which the k = 3 direct sum matches to ~2e-7 (SURVEY 8c pins)."""
+    from gpu_util import GpuRun
+    x, a, s = synth.taylor_green(16)
+    g1 = GpuRun(x, a, s, images=1)
+    u, st = g1.evaluate()
+    u0, s0 = oracle_mod.direct(x, a, x, a, s, images=1)
+    assert oracle_mod.rel_l2(u, u0) <= 1e-3 and oracle_mod.rel_l2(st, s0) <= 1e-3
+    g1.close()
+    g3 = GpuRun(x, a, s, images=3)
+    u, st = g3.evaluate()
+    uc, sc = _tg_closed_form(x.astype(np.float64), a.astype(np.float64), float(s[0]))
+    assert oracle_mod.rel_l2(u, uc) <= 1e-3 and oracle_mod.rel_l2(st, sc) <= 1e-3
+    g3.close()
+
+
+def test_p_sweep_decreases(oracle_mod):
+    from gpu_util import GpuRun
+    x, a, s = synth.random_cloud(4000, seed=1106, sigma=0.05)
+    u0, s0 = oracle_mod.direct(x, a, x, a, s, images=0)
+    eu, es = [], []
+    for p in (4, 6, 8, 10):
+        g = GpuRun(x, a, s, images=0, order=p, ncrit=32)
+        u, st = g.evaluate()
+        eu.append(oracle_mod.rel_l2(u, u0)); es.append(oracle_mod.rel_l2(st, s0))
+        g.close()
+    assert all(b < c for c, b in zip(eu, eu[1:])), eu
+    assert all(b < c for c, b in zip(es, es[1:])), es
+
+
+def test_determinism_and_host_pointers(oracle_mod):
+    import paper_1106_5273_b200 as P
+    from gpu_util import GpuRun
+    x, a, s = synth.taylor_green(20)
+    g = GpuRun(x, a, s, images=3)
+    u1, s1 = g.evaluate()
+    u2, s2 = g.evaluate()
+    assert np.array_equal(u1, u2) and np.array_equal(s1, s2)
+    # same computation from host (pageable numpy) buffers through the same ABI
+    f = P.FMM(images=3)
+    f.set_particles(x, a, s)
+    uh = np.zeros((len(x), 3), dtype=np.float32)
+    sh = np.zeros((len(x), 3), dtype=np.float32)
+    f.evaluate(uh, sh)
+    assert np.array_equal(uh.astype(np.float64), u1) and np.array_equal(sh.astype(np.float64), s1)
+    f.close(); g.close()
+
+
+def test_errors_and_empty():
+    import paper_1106_5273_b200 as P
+    torch = __import__("torch")
+    f = P.FMM(images=3)
+    with pytest.raises(P.FMMError) as e:
+        f.evaluate(np.zeros((1, 3), np.float32), np.zeros((1, 3), np.float32))
+    assert e.value.status == 4                      # FMM_E_STATE
+    x, a, s = synth.taylor_green(4)
+    bad = x.copy(); bad[3, 1] = np.nan
+    with pytest.raises(P.FMMError) as e:
+        f.set_particles(bad, a, s)
+    assert e.value.status == 2                      # FMM_E_NONFINITE
+    s0 = s.copy(); s0[5] = 0.0
+    with pytest.raises(P.FMMError) as e:
+        f.set_particles(x, a, s0)
+    assert e.value.status == 3                      # FMM_E_SIGMA
+    f.set_particles(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32), np.zeros(0, np.float32))
+    f.evaluate(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32))
+    with pytest.raises(P.FMMError) as e:
+        P.FMM(order=1)
+    assert e.value.status == 1                      # FMM_E_ARG
+    f.close()
+
+
+def test_c2_tg64_k3_closed_form_and_sampled_free_space(oracle_mod):
+    """C2 (TG 64^3 = 262k, p = 10, k = 3) vs the closed form at every particle,
+    and the free-space variant vs the double direct sum on 2000 seeded targets."""
+    from gpu_util import GpuRun
+    x, a, s = synth.taylor_green(64)
+    g = GpuRun(x, a, s, images=3)
+    u, st = g.evaluate()
+    uc, sc = _tg_closed_form(x.astype(np.float64), a.astype(np.float64), float(s[0]))
+    assert oracle_mod.rel_l2(u, uc) <= 1e-3 and oracle_mod.rel_l2(st, sc) <= 1e-3
+    g.close()
+    g0 = GpuRun(x, a, s, images=0)
+    u, st = g0.evaluate()
+    idx = np.random.default_rng(1106).choice(len(x), 2000, replace=False)
+    u0, s0 = oracle_mod.direct(x[idx], a[idx], x, a, s, images=0)
+    assert oracle_mod.rel_l2(u[idx], u0) <= 1e-3 and oracle_mod.rel_l2(st[idx], s0) <= 1e-3
+    g0.close()
+
+
+def test_c3_tg256_closed_form_full_size(oracle_mod):
+    """C3 at the bench size (16.8M particles, k = 3, p = 10) in the bench's
+    launch configuration: every particle vs the closed form."""
+    from gpu_util import GpuRun
+    x, a, s = synth.taylor_green(256)
+    g = GpuRun(x, a, s, images=3)
+    u, st = g.evaluate()
+    uc, sc = _tg_closed_form(x.astype(np.float64), a.astype(np.float64), float(s[0]))
+    assert oracle_mod.rel_l2(u, uc) <= 1e-3 and oracle_mod.rel_l2(st, sc) <= 1e-3
+    g.close()
