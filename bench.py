@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark of the FMM evaluation hot path (BASELINE.json metric:
+"FMM eval s/step and sustained FP32 TFLOP/s at N particles, 1/2/4/8 B200").
+
+One step = fmm_set_particles (wrap, Morton keys, radix sort, octree) +
+fmm_evaluate (P2M, M2M, traversal, M2L, periodic far field, P2P, L2L, L2P,
+un-permute): every row of SURVEY 8(a), through the C ABI.
+
+Workload (N = 1): C3 -- Taylor-Green 256^3 = 16.8M particles, periodic
+[-pi, pi)^3 with k = 3 image layers, p = 10, theta = 1/2, ncrit = 64 (the
+BASELINE config quoted for "full step timing", and the paper's per-GPU size,
+P:243/P:284).  Inputs are resident in HBM before the timed region; they are
+larger than the 126 MB L2 (470 MB), so no explicit flush is needed.
+
+value = paper-style sustained FP32 TFLOP/s = 174 x (P2P pairs) / step time,
+summed over ranks (Table 1 and the flop formula).
+e2e   = the same metric with host (pinned) inputs/outputs through the C ABI,
+        host<->device copies inside the timed region.
+
+--impl reference times the CPU oracle (test infrastructure) on a bounded
+sample of the same workload family.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "FMM eval s/step and sustained FP32 TFLOP/s at N particles, 1/2/4/8 B200"
+FLOPS_PER_PAIR = 174          # Table 1: 70 Biot-Savart + 104 stretching
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x FMA x max SM clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=256, help="lattice points per dimension per GPU")
+    ap.add_argument("--order", type=int, default=10)
+    ap.add_argument("--images", type=int, default=3)
+    ap.add_argument("--theta", default="1/2")
+    ap.add_argument("--ncrit", type=int, default=64)
+    ap.add_argument("--cpu-sample", type=int, default=32, help="oracle sample: TG n^3 lattice")
+    ap.add_argument("--ref-sample", type=int, default=24, help="--impl reference sample: TG n^3 lattice")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def theta_of(s):
+    a, b = s.split("/")
+    return int(a), int(b)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                self.rows.append(p)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------ CPU oracle --
+def oracle_step(n, order, images, theta, ncrit):
+    """One oracle FMM step (tree, traversal, evaluation) on TG n^3; returns
+    (seconds, p2p pairs)."""
+    import oracle
+    import synth
+    x, a, s = synth.taylor_green(n)
+    t0 = time.perf_counter()
+    f = oracle.OracleFMM(x, a, s, order=order, theta=theta, ncrit=ncrit, images=images)
+    f.evaluate()
+    dt = time.perf_counter() - t0
+    cells = f.cells()
+    p2p = f.p2p_list()
+    pairs = int(np.sum(cells[p2p[:, 0], 5].astype(np.int64) * cells[p2p[:, 1], 5].astype(np.int64)))
+    return dt, pairs
+
+
+def cpu_baseline(args, theta):
+    import oracle
+    oracle.build()
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    dt, pairs = oracle_step(args.cpu_sample, args.order, args.images, theta, args.ncrit)
+    return {"value": FLOPS_PER_PAIR * pairs / dt / 1e12, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "oracle",
+            "sample": "oracle FMM step (double, OpenMP) on Taylor-Green %d^3 = %d particles, same p/theta/ncrit/k; "
+                      "%.2f s, %d P2P pairs" % (args.cpu_sample, args.cpu_sample ** 3, dt, pairs)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    theta = theta_of(args.theta)
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    for _ in range(args.warmup):
+        oracle_step(args.ref_sample, args.order, args.images, theta, args.ncrit)
+    ts, pairs = [], 0
+    for _ in range(args.steps):
+        dt, pairs = oracle_step(args.ref_sample, args.order, args.images, theta, args.ncrit)
+        ts.append(dt)
+    tot = sum(ts)
+    v = FLOPS_PER_PAIR * pairs * len(ts) / tot / 1e12
+    sample = ("oracle FMM step (double, OpenMP) on Taylor-Green %d^3 = %d particles per step, p=%d, k=%d, "
+              "theta=%s, ncrit=%d" % (args.ref_sample, args.ref_sample ** 3, args.order, args.images, args.theta,
+                                      args.ncrit))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Taylor-Green lattice",
+        "config": {"workload": "C3 family (bounded CPU sample)", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# -------------------------------------------------------------- our arm --
+def load_profile_traffic():
+    """dram bytes per P2P launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "latest_p2p.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_1106_5273_b200 as P
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    theta = theta_of(args.theta)
+
+    x, a, s = synth.taylor_green(args.n)
+    n = len(x)
+    stream = torch.cuda.Stream()
+    f = P.FMM(order=args.order, images=args.images, theta=theta, ncrit=args.ncrit, device=local,
+              stream=stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
+        ud = torch.empty((n, 3), device="cuda")
+        dd = torch.empty((n, 3), device="cuda")
+
+    def step():
+        f.set_particles(xd, ad, sd)
+        f.evaluate(ud, dd)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step()
+    barrier()
+
+    gpu_index = local
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if cvd:
+        try:
+            gpu_index = int(cvd.split(",")[local])
+        except Exception:
+            pass
+    clk = ClockSampler(gpu_index)
+    clk.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+            stats.append(f.stats())
+        e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+
+    pairs = stats[-1]["p2p_pairs"]
+    launches = sum(st["launches"] for st in stats)
+    cub_calls = sum(st["cub_calls"] for st in stats)
+    phase = {k: statistics.mean(st[k] for st in stats) for k in
+             ("ms_keys", "ms_sort", "ms_tree", "ms_upward", "ms_traverse", "ms_m2l", "ms_p2p", "ms_downward",
+              "ms_finalize", "ms_set_total", "ms_eval_total")}
+
+    # e2e through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh, ah, sh = (torch.from_numpy(v).pin_memory() for v in (x, a, s))
+        uh = torch.empty((n, 3)).pin_memory()
+        dh = torch.empty((n, 3)).pin_memory()
+        ke = max(3, args.steps // 2)
+        with torch.cuda.stream(stream):
+            f.set_particles(xh, ah, sh)
+            f.evaluate(uh, dh)
+        barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(ke):
+                f.set_particles(xh, ah, sh)
+                f.evaluate(uh, dh)
+            e1.record(stream)
+        barrier()
+        wall = (time.perf_counter() - t0) / ke
+        ms_e2e = max(e0.elapsed_time(e1) / ke, 1e3 * wall)
+        e2e = {"ms_per_step": ms_e2e, "h2d_bytes_per_step": int(xh.numel() * 4 + ah.numel() * 4 + sh.numel() * 4),
+               "d2h_bytes_per_step": int(uh.numel() * 4 + dh.numel() * 4), "pairs": pairs}
+
+    # aggregate over ranks: max time, summed work
+    t = torch.tensor([ms, e2e["ms_per_step"] if e2e else 0.0, phase["ms_p2p"]], dtype=torch.float64, device="cuda")
+    w = torch.tensor([float(pairs), float(n)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    ms_max, ms_e2e_max, p2p_ms_max = t.tolist()
+    tot_pairs, tot_n = w.tolist()
+    value = FLOPS_PER_PAIR * tot_pairs / (ms_max * 1e-3) / 1e12
+
+    if rank == 0:
+        traffic, prof = load_profile_traffic()
+        achieved = FLOPS_PER_PAIR * pairs / (phase["ms_p2p"] * 1e-3) / 1e12
+        roof = {"kernel": "k_p2p (near field, a12)", "bound": "alu", "achieved": achieved,
+                "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                "traffic": traffic,
+                "note": "achieved = 174 model flop/pair (Table 1) x pairs / mean P2P launch time (CUDA events on the "
+                        "launch stream); peak = 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"}
+        if prof:
+            roof["hw"] = {k: prof[k] for k in prof if k != "dram_bytes_per_launch"}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(args, theta)
+            except Exception as ex:  # the baseline never blocks the GPU number
+                cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
+                       "sample": "failed: %s" % ex}
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_max, "s_per_step": ms_max / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic Taylor-Green lattice (reading Z26), generated on host, resident in HBM",
+            "config": {"workload": "C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
+                                   "ncrit=%d" % (args.n, n, args.images, args.order, args.theta, args.ncrit),
+                       "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
+                       "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),
+                       "parallelism": "1 GPU" if world == 1 else
+                       "%d independent periodic replicas (LET exchange not yet implemented)" % world},
+            "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
+            "particles_per_s": tot_n / (ms_max * 1e-3),
+            "phases_ms": phase,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": None if not e2e else {
+                "value": FLOPS_PER_PAIR * tot_pairs / (ms_e2e_max * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "ms_per_step": ms_e2e_max, "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]},
+            "gpu_launches": int(launches), "cub_calls": int(cub_calls),
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,8 @@ typedef struct {
   int64_t  p2p_pairs;            /* particle pairs evaluated by P2P                    */
   int64_t  far_m2l;              /* M2L of the periodic far layers (a8)                */
   double   model_flops;          /* 174 * p2p_pairs (Table 1)               */
+  int64_t  launches;             /* this library's kernel launches since set_particles */
+  int64_t  cub_calls;            /* CUB device-wide calls (radix sort, scan) since then */
   double   ms_keys, ms_sort, ms_tree;                  /* set_particles: a1-a4         */
   double   ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_downward, ms_finalize;
   double   ms_set_total, ms_eval_total;

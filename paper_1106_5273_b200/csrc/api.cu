@@ -115,7 +115,7 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   if (hs) { c.stage_ds.reserve(3 * n); ds = c.stage_ds.p; }
   unsigned g = nblocks(n, 256);
   if (g > 148 * 16) g = 148 * 16;
-  k_finalize<<<g, 256, 0, st>>>(c.idx.p, n, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
+  FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
   FMM_LAUNCH_CHECK();
   if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
   if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
@@ -262,6 +262,8 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->p2p_pairs = c.p2p_pairs;
   s->far_m2l = c.far_m2l;
   s->model_flops = 174.0 * (double)c.p2p_pairs;
+  s->launches = c.launches;
+  s->cub_calls = c.cub_calls;
   return FMM_OK;
 }
 

@@ -32,6 +32,15 @@ struct FmmError : std::runtime_error {
 
 #define FMM_LAUNCH_CHECK() FMM_CUDA(cudaGetLastError())
 
+// Launch one of this library's kernels on the context stream and count it
+// (fmm_stats.launches: the bench's gpu_launches claim).
+#define FMM_LAUNCH(ctx, kern, grid, block, smem, ...)                  \
+  do {                                                                 \
+    kern<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);      \
+    ++(ctx).launches;                                                  \
+    FMM_CUDA(cudaGetLastError());                                      \
+  } while (0)
+
 // Grow-only device buffer owned by a context.
 template <typename T>
 struct DBuf {

@@ -61,6 +61,9 @@ struct Ctx {
   bool evaluated = false;
   int64_t far_m2l = 0;
 
+  // ---- counters ----
+  int64_t launches = 0, cub_calls = 0;       // since the last set_particles
+
   // ---- timing ----
   cudaEvent_t ev[PH_N + 1] = {};
   fmm_stats stats{};
@@ -71,6 +74,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
 void build_lists(Ctx& c);
 void upward_pass(Ctx& c);
 void m2l_pass(Ctx& c);
+bool m2l_pass_reg(Ctx& c);
 void periodic_far_pass(Ctx& c);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);

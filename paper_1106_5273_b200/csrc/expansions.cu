@@ -124,7 +124,7 @@ __global__ void k_m2l(int P, int64_t ncells, const int* __restrict__ seg_b, cons
                       float2* __restrict__ Lc) {
   extern __shared__ float2 sm[];
   const int nc = P * (P + 1) / 2;
-  const int P2 = 2 * P - 1;
+  const int P2 = P;   // I_j for j = n + k <= p - 1
   const int nc2 = P2 * (P2 + 1) / 2;
   cpx<float>* Is = (cpx<float>*)sm;            // [nc2]
   cpx<float>* Ms = (cpx<float>*)(sm + nc2);    // [3][nc]
@@ -225,7 +225,7 @@ __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, GCells 
                           const double* __restrict__ farM, float2* __restrict__ Lc) {
   extern __shared__ double smd[];
   const int nc = P * (P + 1) / 2;
-  const int P2 = 2 * P - 1;
+  const int P2 = P;   // I_j for j = n + k <= p - 1
   const int nc2 = P2 * (P2 + 1) / 2;
   cpx<double>* Is = (cpx<double>*)smd;          // [nc2]
   cpx<double>* Ms = Is + nc2;                   // [3][nc]
@@ -407,23 +407,24 @@ void upward_pass(Ctx& c) {
   GCells gc = gcells(c);
   if (c.nleaves > 0) {
     size_t sm = sizeof(float2) * (32 * nc) + sizeof(float4) * 32;
-    k_p2m<<<(unsigned)c.nleaves, round32(3 * nc), sm, st>>>(P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
+    FMM_LAUNCH(c, k_p2m, (unsigned)c.nleaves, round32(3 * nc), sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
     FMM_LAUNCH_CHECK();
   }
   int nlev = (int)c.level_begin.size() - 1;
   for (int l = nlev - 2; l >= 0; --l) {
     int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
     if (cnt <= 0) continue;
-    k_m2m<<<(unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, st>>>(P, first, gc, c.M.p);
+    FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, P, first, gc, c.M.p);
     FMM_LAUNCH_CHECK();
   }
 }
 
 void m2l_pass(Ctx& c) {
   if (c.nm2l == 0) return;
-  int P = c.P, nc = c.nc, P2 = 2 * P - 1, nc2 = P2 * (P2 + 1) / 2;
+  if (m2l_pass_reg(c)) return;   // register-blocked kernel (m2l.cu) for p in {4, 6, 8, 10}
+  int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   size_t sm = sizeof(float2) * (nc2 + 3 * nc);
-  k_m2l<<<(unsigned)c.ncells, round32(nc), sm, c.stream>>>(P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), c.M.p,
+  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), c.M.p,
                                                           c.Lc.p);
   FMM_LAUNCH_CHECK();
 }
@@ -432,7 +433,7 @@ void periodic_far_pass(Ctx& c) {
   int k = c.cfg.images;
   c.far_m2l = 0;
   if (k < 2 || c.ncells == 0) return;
-  int P = c.P, nc = c.nc, P2 = 2 * P - 1, nc2 = P2 * (P2 + 1) / 2;
+  int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   // far targets: cells at level 2 and leaves above level 2
   std::vector<int> tg;
   for (size_t i = 0; i < c.host_leaf_top.size(); ++i)
@@ -440,12 +441,12 @@ void periodic_far_pass(Ctx& c) {
   if (c.level_begin.size() > 3)
     for (int64_t i = c.level_begin[2]; i < c.level_begin[3]; ++i) tg.push_back((int)i);
   c.far_M.reserve((size_t)(k - 1) * 3 * nc * 2);
-  k_far_super<<<1, round32(3 * nc), sizeof(double) * 2 * nc, c.stream>>>(P, k, c.M.p, c.far_M.p);
+  FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, c.M.p, c.far_M.p);
   FMM_LAUNCH_CHECK();
   c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
   FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
   size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
-  k_far_m2l<<<(unsigned)tg.size(), round32(nc), sm, c.stream>>>(P, k, c.scan.p, gcells(c), geo(c), c.far_M.p, c.Lc.p);
+  FMM_LAUNCH(c, k_far_m2l, (unsigned)tg.size(), round32(nc), sm, P, k, c.scan.p, gcells(c), geo(c), c.far_M.p, c.Lc.p);
   FMM_LAUNCH_CHECK();
   c.far_m2l = (int64_t)tg.size() * 702 * (k - 1);
 }
@@ -458,12 +459,12 @@ void downward_pass(Ctx& c, float* u_far, float* s_far) {
   for (int l = 1; l < nlev; ++l) {
     int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
     if (cnt <= 0) continue;
-    k_l2l<<<(unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, st>>>(P, first, gc, c.Lc.p);
+    FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, c.Lc.p);
     FMM_LAUNCH_CHECK();
   }
   if (c.nleaves > 0) {
     size_t sm = sizeof(float2) * (3 * nc + 32 * nc);
-    k_l2p<<<(unsigned)c.nleaves, 32, sm, st>>>(P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.Lc.p, u_far, s_far);
+    FMM_LAUNCH(c, k_l2p, (unsigned)c.nleaves, 32, sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.Lc.p, u_far, s_far);
     FMM_LAUNCH_CHECK();
   }
 }

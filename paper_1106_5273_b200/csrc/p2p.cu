@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(TP) k_p2p(const int* __restrict__ leaf_ids, co
 void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   if (c.nleaves == 0) return;
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
-  k_p2p<<<(unsigned)c.nleaves, TP, 0, c.stream>>>(c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
+  FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, TP, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
                                                   c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near);
   FMM_LAUNCH_CHECK();
 }

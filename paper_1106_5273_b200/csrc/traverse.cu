@@ -111,6 +111,7 @@ void cub_call(Ctx& c, F f) {
   FMM_CUDA(f((void*)nullptr, bytes));
   c.cub_tmp.reserve(bytes);
   FMM_CUDA(f((void*)c.cub_tmp.p, bytes));
+  ++c.cub_calls;
 }
 
 void exclusive_scan(Ctx& c, const int* in, int* out, int64_t n) {
@@ -168,7 +169,7 @@ void build_lists(Ctx& c) {
     c.cnt_m2l.reserve(nf + 1); c.cnt_p2p.reserve(nf + 1); c.cnt_push.reserve(nf + 1);
     c.off_m2l.reserve(nf + 1); c.off_p2p.reserve(nf + 1); c.off_push.reserve(nf + 1);
     unsigned g = nblocks(nf, 256);
-    k_expand<false><<<g, 256, 0, st>>>(c.front_a.p, nf, tc, tp, c.cnt_m2l.p, c.cnt_p2p.p, c.cnt_push.p,
+    FMM_LAUNCH(c, k_expand<false>, g, 256, 0, c.front_a.p, nf, tc, tp, c.cnt_m2l.p, c.cnt_p2p.p, c.cnt_push.p,
                                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     FMM_LAUNCH_CHECK();
     exclusive_scan(c, c.cnt_m2l.p, c.off_m2l.p, nf);
@@ -188,7 +189,7 @@ void build_lists(Ctx& c) {
     c.m2l.grow_keep(c.nm2l + add_m, c.nm2l, st);
     c.p2p.grow_keep(c.np2p + add_p, c.np2p, st);
     c.front_b.reserve(add_q);
-    k_expand<true><<<g, 256, 0, st>>>(c.front_a.p, nf, tc, tp, nullptr, nullptr, nullptr, c.off_m2l.p,
+    FMM_LAUNCH(c, k_expand<true>, g, 256, 0, c.front_a.p, nf, tc, tp, nullptr, nullptr, nullptr, c.off_m2l.p,
                                       c.off_p2p.p, c.off_push.p, c.m2l.p + c.nm2l, c.p2p.p + c.np2p, c.front_b.p);
     FMM_LAUNCH_CHECK();
     c.nm2l += add_m;
@@ -203,16 +204,16 @@ void build_lists(Ctx& c) {
   sort_list(c, c.m2l, c.nm2l);
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
   c.m2l_b.reserve(c.ncells); c.m2l_e.reserve(c.ncells);
-  k_clear2<<<nblocks(c.ncells, 256), 256, 0, st>>>(c.p2p_b.p, c.p2p_e.p, c.ncells);
-  k_clear2<<<nblocks(c.ncells, 256), 256, 0, st>>>(c.m2l_b.p, c.m2l_e.p, c.ncells);
-  if (c.np2p) k_segments<<<nblocks(c.np2p, 256), 256, 0, st>>>(c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
-  if (c.nm2l) k_segments<<<nblocks(c.nm2l, 256), 256, 0, st>>>(c.m2l.p, c.nm2l, c.m2l_b.p, c.m2l_e.p);
+  FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
+  FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.m2l_b.p, c.m2l_e.p, c.ncells);
+  if (c.np2p) FMM_LAUNCH(c, k_segments, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
+  if (c.nm2l) FMM_LAUNCH(c, k_segments, nblocks(c.nm2l, 256), 256, 0, c.m2l.p, c.nm2l, c.m2l_b.p, c.m2l_e.p);
   c.dcount.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
   if (c.np2p) {
     unsigned g = nblocks(c.np2p, 256);
     if (g > 148 * 8) g = 148 * 8;
-    k_pair_count<<<g, 256, 0, st>>>(c.p2p.p, c.np2p, c.cells.count.p, c.dcount.p);
+    FMM_LAUNCH(c, k_pair_count, g, 256, 0, c.p2p.p, c.np2p, c.cells.count.p, c.dcount.p);
   }
   FMM_LAUNCH_CHECK();
   unsigned long long pairs = 0;

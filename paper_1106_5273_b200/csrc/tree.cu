@@ -211,6 +211,7 @@ void cub_call(Ctx& c, F f) {
   FMM_CUDA(f((void*)nullptr, bytes));
   c.cub_tmp.reserve(bytes);
   FMM_CUDA(f((void*)c.cub_tmp.p, bytes));
+  ++c.cub_calls;
 }
 
 }  // namespace
@@ -223,6 +224,8 @@ static unsigned grid_for(int64_t n) {
 void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const float* s) {
   cudaStream_t st = c.stream;
   c.n = n;
+  c.launches = 0;
+  c.cub_calls = 0;
   c.have_particles = false;
   c.lists_valid = false;
   c.evaluated = false;
@@ -237,7 +240,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   FMM_CUDA(cudaMemcpyAsync(c.dflag.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
   int periodic = c.cfg.images > 0;
   if (n > 0) {
-    k_validate<<<grid_for(n), 256, 0, st>>>(x, a, s, n, c.dflag.p, !periodic);
+    FMM_LAUNCH(c, k_validate, grid_for(n), 256, 0, x, a, s, n, c.dflag.p, !periodic);
     FMM_LAUNCH_CHECK();
   }
   int h[8];
@@ -277,7 +280,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   // a2: keys
   c.pos_tmp.reserve(n); c.keys_tmp.reserve(n); c.idx_tmp.reserve(n);
   c.keys.reserve(n); c.idx.reserve(n); c.pos.reserve(n); c.alp.reserve(n);
-  k_keys<<<grid_for(n), 256, 0, st>>>(x, s, n, b, c.pos_tmp.p, c.keys_tmp.p, c.idx_tmp.p);
+  FMM_LAUNCH(c, k_keys, grid_for(n), 256, 0, x, s, n, b, c.pos_tmp.p, c.keys_tmp.p, c.idx_tmp.p);
   FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaEventRecord(c.ev[PH_KEYS], st));
 
@@ -290,7 +293,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
       return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, nn, 0, 63, st);
     });
   }
-  k_gather<<<grid_for(n), 256, 0, st>>>(c.pos_tmp.p, a, c.idx.p, n, c.pos.p, c.alp.p);
+  FMM_LAUNCH(c, k_gather, grid_for(n), 256, 0, c.pos_tmp.p, a, c.idx.p, n, c.pos.p, c.alp.p);
   FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaEventRecord(c.ev[PH_SORT], st));
 
@@ -298,15 +301,15 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   size_t capc = (size_t)(2 * (n / (c.cfg.ncrit + 1)) + 64);
   c.cells.reserve_keep(capc, 0, st);
   c.pcell_a.reserve(n); c.pcell_b.reserve(n); c.flags.reserve(n); c.scan.reserve(n);
-  k_root<<<1, 1, 0, st>>>(ptrs(c.cells), n, c.cfg.ncrit);
-  k_fill_int<<<grid_for(n), 256, 0, st>>>(c.pcell_a.p, n, 0);
+  FMM_LAUNCH(c, k_root, 1, 1, 0, ptrs(c.cells), n, c.cfg.ncrit);
+  FMM_LAUNCH(c, k_fill_int, grid_for(n), 256, 0, c.pcell_a.p, n, 0);
   FMM_LAUNCH_CHECK();
   int64_t ncells = 1;
   c.level_begin.assign({0, 1});
   int* pc_old = c.pcell_a.p;
   int* pc_new = c.pcell_b.p;
   for (int l = 1; l <= kMaxLevel; ++l) {
-    k_level_flags<<<grid_for(n), 256, 0, st>>>(c.keys.p, pc_old, c.cells.leaf.p, n, l, c.flags.p);
+    FMM_LAUNCH(c, k_level_flags, grid_for(n), 256, 0, c.keys.p, pc_old, c.cells.leaf.p, n, l, c.flags.p);
     FMM_LAUNCH_CHECK();
     {
       int* fin = c.flags.p;
@@ -321,9 +324,9 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
     FMM_CUDA(cudaStreamSynchronize(st));
     if (total == 0) break;
     if ((size_t)(ncells + total) > c.cells.level.cap) c.cells.reserve_keep((size_t)(ncells + total) * 2, ncells, st);
-    k_level_fill<<<grid_for(n), 256, 0, st>>>(c.keys.p, pc_old, c.flags.p, c.scan.p, ptrs(c.cells), n, l,
+    FMM_LAUNCH(c, k_level_fill, grid_for(n), 256, 0, c.keys.p, pc_old, c.flags.p, c.scan.p, ptrs(c.cells), n, l,
                                               (int)ncells, pc_new);
-    k_level_end<<<grid_for(n), 256, 0, st>>>(pc_new, ptrs(c.cells), n, l, c.cfg.ncrit);
+    FMM_LAUNCH(c, k_level_end, grid_for(n), 256, 0, pc_new, ptrs(c.cells), n, l, c.cfg.ncrit);
     FMM_LAUNCH_CHECK();
     ncells += total;
     c.level_begin.push_back(ncells);
@@ -334,7 +337,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
 
   // leaf id list
   c.leaf_ids.reserve(ncells);
-  k_leaf_flags<<<grid_for(ncells), 256, 0, st>>>(c.cells.leaf.p, ncells, c.flags.p);
+  FMM_LAUNCH(c, k_leaf_flags, grid_for(ncells), 256, 0, c.cells.leaf.p, ncells, c.flags.p);
   {
     int* fin = c.flags.p;
     int* fout = c.scan.p;
@@ -343,7 +346,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
       return cub::DeviceScan::InclusiveSum(tmp, bytes, fin, fout, nn, st);
     });
   }
-  k_scatter_leaves<<<grid_for(ncells), 256, 0, st>>>(c.cells.leaf.p, c.scan.p, ncells, c.leaf_ids.p);
+  FMM_LAUNCH(c, k_scatter_leaves, grid_for(ncells), 256, 0, c.cells.leaf.p, c.scan.p, ncells, c.leaf_ids.p);
   FMM_LAUNCH_CHECK();
   int nl = 0;
   FMM_CUDA(cudaMemcpyAsync(&nl, c.scan.p + (ncells - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
