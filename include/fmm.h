@@ -139,6 +139,11 @@ fmm_status fmm_get_lists(fmm_ctx* ctx, int64_t* p2p, int64_t* m2l);
  * (interleaved re, im) -- either pointer may be NULL. */
 fmm_status fmm_get_expansions(const fmm_ctx* ctx, float* M, float* L);
 
+/* The device's FP32 evaluation of the Eq. 2 cutoff g(rho) used by P2P
+ * (reading Z6: any approximation with |g - g_exact| <= 2e-7).  rho[n] in,
+ * g[n] out; host or device pointers.  Used by the parity tests. */
+fmm_status fmm_eval_cutoff(fmm_ctx* ctx, int64_t n, const float* rho, float* g);
+
 #ifdef __cplusplus
 }
 #endif

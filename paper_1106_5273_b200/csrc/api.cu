@@ -349,3 +349,20 @@ FMM_API fmm_status fmm_get_expansions(const fmm_ctx* h, float* M, float* L) {
     if (L && bytes) FMM_CUDA(cudaMemcpy(L, c.Lc.p, bytes, cudaMemcpyDeviceToHost));
   });
 }
+
+FMM_API fmm_status fmm_eval_cutoff(fmm_ctx* h, int64_t n, const float* rho, float* g) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (n < 0 || (n > 0 && (!rho || !g))) throw FmmError(FMM_E_ARG, "bad arguments");
+    if (n == 0) return;
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    c.stage_u.reserve(n);
+    c.stage_ds.reserve(n);
+    FMM_CUDA(cudaMemcpyAsync(c.stage_u.p, rho, sizeof(float) * n, cudaMemcpyDefault, c.stream));
+    eval_cutoff(c, c.stage_u.p, n, c.stage_ds.p);
+    FMM_CUDA(cudaMemcpyAsync(g, c.stage_ds.p, sizeof(float) * n, cudaMemcpyDefault, c.stream));
+    FMM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}

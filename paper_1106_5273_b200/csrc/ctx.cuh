@@ -56,6 +56,7 @@ struct Ctx {
   // ---- expansions and results ----
   DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)
   DBuf<double> far_M;                        // periodic super-cell multipoles
+  DBuf<double2> far_part;                    // per-chunk partial far-field locals
   DBuf<float> u_near, s_near, u_far, s_far;  // sorted order, [n][3]
   DBuf<float> stage_u, stage_ds;             // host-output staging
   bool evaluated = false;
@@ -78,6 +79,7 @@ bool m2l_pass_reg(Ctx& c);
 void periodic_far_pass(Ctx& c);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);
+void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g);
 
 }  // namespace fmmb
 

@@ -221,8 +221,11 @@ __global__ void k_far_super(int P, int k, const float2* __restrict__ Mroot, doub
   }
 }
 
-__global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, GCells c, Geo g,
-                          const double* __restrict__ farM, float2* __restrict__ Lc) {
+// block (x = target, y = chunk): chunk = (layer j - 1) * 26 + (neighbour I != 0);
+// the 27 children C of that neighbour are summed here, the chunks are summed
+// in a fixed order by k_far_reduce (deterministic).
+__global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, int ntg, GCells c, Geo g,
+                          const double* __restrict__ farM, double2* __restrict__ part) {
   extern __shared__ double smd[];
   const int nc = P * (P + 1) / 2;
   const int P2 = P;   // I_j for j = n + k <= p - 1
@@ -230,56 +233,69 @@ __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, GCells 
   cpx<double>* Is = (cpx<double>*)smd;          // [nc2]
   cpx<double>* Ms = Is + nc2;                   // [3][nc]
   const cpx<double>* F = (const cpx<double>*)farM;
-  int t = targets[blockIdx.x];
-  int lt = c.level[t];
-  double st = g.L / (double)(1 << lt);
-  double rx = (c.qx[t] + 0.5) * st - 0.5 * g.L, ry = (c.qy[t] + 0.5) * st - 0.5 * g.L,
-         rz = (c.qz[t] + 0.5) * st - 0.5 * g.L;   // c_t - c_0
+  const int t = targets[blockIdx.x];
+  const int chunk = blockIdx.y;
+  const int j = 1 + chunk / 26;
+  int I3 = chunk % 26;
+  if (I3 >= kImgCentre) ++I3;
+  const int lt = c.level[t];
+  const double st = g.L / (double)(1 << lt);
+  const double rx = (c.qx[t] + 0.5) * st - 0.5 * g.L, ry = (c.qy[t] + 0.5) * st - 0.5 * g.L,
+               rz = (c.qz[t] + 0.5) * st - 0.5 * g.L;   // c_t - c_0
   int kq = 0, lq = 0;
   if ((int)threadIdx.x < nc) nm_of(threadIdx.x, kq, lq);
   cpx<double> acc[3] = {{0, 0}, {0, 0}, {0, 0}};
   double scale = g.L;
-  for (int j = 1; j < k; ++j, scale *= 3.0) {
-    double ratio = scale / st;
-    for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
-      int kk = i % nc, n, m;
-      nm_of(kk, n, m);
-      double sc = pow(ratio, n);
-      cpx<double> v = F[(j - 1) * 3 * nc + i];
-      Ms[i] = {v.re * sc, v.im * sc};
-    }
-    for (int I3 = 0; I3 < 27; ++I3) {
-      if (I3 == kImgCentre) continue;
-      for (int C3 = 0; C3 < 27; ++C3) {
-        double ox = 3 * (I3 % 3 - 1) + (C3 % 3 - 1), oy = 3 * ((I3 / 3) % 3 - 1) + ((C3 / 3) % 3 - 1),
-               oz = 3 * (I3 / 9 - 1) + (C3 / 9 - 1);
-        double Dx = (rx - ox * scale) / st, Dy = (ry - oy * scale) / st, Dz = (rz - oz * scale) / st;
-        __syncthreads();
-        for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<double>(Dx, Dy, Dz, m, P2, Is);
-        __syncthreads();
-        if ((int)threadIdx.x < nc) {
-          for (int n = P - 1 - kq; n >= 0; --n)
-            for (int m = -n; m <= n; ++m) {
-              cpx<double> I = cget(Is, n + kq, m + lq);
-              for (int comp = 0; comp < 3; ++comp) {
-                cpx<double> Mv = cget(Ms + comp * nc, n, m);
-                acc[comp].re += Mv.re * I.re - Mv.im * I.im;
-                acc[comp].im += Mv.re * I.im + Mv.im * I.re;
-              }
-            }
-        }
-      }
-    }
+  for (int jj = 1; jj < j; ++jj) scale *= 3.0;
+  const double ratio = scale / st;
+  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+    int kk = i % nc, n, m;
+    nm_of(kk, n, m);
+    double sc = pow(ratio, n);
+    cpx<double> v = F[(j - 1) * 3 * nc + i];
+    Ms[i] = {v.re * sc, v.im * sc};
+  }
+  for (int C3 = 0; C3 < 27; ++C3) {
+    double ox = 3 * (I3 % 3 - 1) + (C3 % 3 - 1), oy = 3 * ((I3 / 3) % 3 - 1) + ((C3 / 3) % 3 - 1),
+           oz = 3 * (I3 / 9 - 1) + (C3 / 9 - 1);
+    double Dx = (rx - ox * scale) / st, Dy = (ry - oy * scale) / st, Dz = (rz - oz * scale) / st;
     __syncthreads();
+    for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<double>(Dx, Dy, Dz, m, P2, Is);
+    __syncthreads();
+    if ((int)threadIdx.x < nc) {
+      for (int n = P - 1 - kq; n >= 0; --n)
+        for (int m = -n; m <= n; ++m) {
+          cpx<double> I = cget(Is, n + kq, m + lq);
+          for (int comp = 0; comp < 3; ++comp) {
+            cpx<double> Mv = cget(Ms + comp * nc, n, m);
+            acc[comp].re += Mv.re * I.re - Mv.im * I.im;
+            acc[comp].im += Mv.re * I.im + Mv.im * I.re;
+          }
+        }
+    }
   }
   if ((int)threadIdx.x < nc) {
-    double sg = (kq & 1) ? -1.0 : 1.0;
-    for (int comp = 0; comp < 3; ++comp) {
-      float2* d = Lc + ((int64_t)t * 3 + comp) * nc + threadIdx.x;
-      float2 v = *d;
-      *d = make_float2((float)((double)v.x + sg * acc[comp].re), (float)((double)v.y + sg * acc[comp].im));
-    }
+    const double sg = (kq & 1) ? -1.0 : 1.0;
+    for (int comp = 0; comp < 3; ++comp)
+      part[((int64_t)chunk * ntg + blockIdx.x) * 3 * nc + comp * nc + threadIdx.x] =
+          make_double2(sg * acc[comp].re, sg * acc[comp].im);
   }
+}
+
+__global__ void k_far_reduce(int nc, int nchunk, const int* __restrict__ targets, int ntg,
+                             const double2* __restrict__ part, float2* __restrict__ Lc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntg * 3 * nc) return;
+  const int ti = i / (3 * nc), o = i - ti * 3 * nc;
+  double sr = 0, si = 0;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const double2 v = part[((int64_t)ch * ntg + ti) * 3 * nc + o];
+    sr += v.x;
+    si += v.y;
+  }
+  float2* d = Lc + (int64_t)targets[ti] * 3 * nc + o;
+  const float2 old = *d;
+  *d = make_float2((float)((double)old.x + sr), (float)((double)old.y + si));
 }
 
 // ---------------------------------------------------------------- L2L (a10)
@@ -446,7 +462,12 @@ void periodic_far_pass(Ctx& c) {
   c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
   FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
   size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
-  FMM_LAUNCH(c, k_far_m2l, (unsigned)tg.size(), round32(nc), sm, P, k, c.scan.p, gcells(c), geo(c), c.far_M.p, c.Lc.p);
+  const int ntg = (int)tg.size(), nchunk = 26 * (k - 1);
+  c.far_part.reserve((size_t)nchunk * ntg * 3 * nc);
+  FMM_LAUNCH(c, k_far_m2l, dim3(ntg, nchunk), round32(nc), sm, P, k, c.scan.p, ntg, gcells(c), geo(c), c.far_M.p,
+             c.far_part.p);
+  FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)ntg * 3 * nc, 128), 128, 0, nc, nchunk, c.scan.p, ntg, c.far_part.p,
+             c.Lc.p);
   FMM_LAUNCH_CHECK();
   c.far_m2l = (int64_t)tg.size() * 702 * (k - 1);
 }

@@ -13,8 +13,9 @@
 // Per source the 55 irregular harmonics I_j^m(D/s_t), j <= p-1, are built once,
 // column-parallel across the warp, into shared memory; the fully unrolled
 // accumulation then reads each I_j^m exactly once and issues the 1210
-// complex multiply-adds per component as straight FFMA chains with all
-// indices, conjugations and signs resolved at compile time.  The ten
+// complex multiply-adds per component as packed FP32x2 FMAs (FFMA2, two per
+// complex MAC, the scalar M parts broadcast) with all indices, conjugations
+// and signs resolved at compile time.  The ten
 // subsets' partial locals are reduced in a fixed order at the end
 // (deterministic), so no float atomics are used.
 #include <type_traits>
@@ -38,15 +39,16 @@ struct Dims {
   static constexpr int NC = P * (P + 1) / 2;
   static constexpr int P2 = P;                    // M2L needs I_j for j = n + k <= p - 1 only
   static constexpr int NC2 = P2 * (P2 + 1) / 2;
-  static constexpr int S = (NC2 & 1) ? NC2 : NC2 + 1;   // odd stride (float2) => conflict-free subsets
+  // per source: 2 float4 per (j, m) = {I, (-Im, Re)} and {I^{-m}, (-Im, Re) of I^{-m}}; the
+  // stride (float4 units) is 7 mod 8 so the ten subsets spread over the 8 bank groups
+  static constexpr int S = 2 * NC2 + ((7 - (2 * NC2) % 8) + 8) % 8;
 };
 
-// acc += A * B (complex), every sign a compile-time constant
-__device__ __forceinline__ void cmac(float& xr, float& xi, float ar, float ai, float br, float bi) {
-  xr = fmaf(ar, br, xr);
-  xr = fmaf(-ai, bi, xr);
-  xi = fmaf(ar, bi, xi);
-  xi = fmaf(ai, br, xi);
+// acc += a * B + b * B' with scalar a, b broadcast into both FP32 lanes:
+// two FFMA2 (packed FP32x2 FMA, sm_100a) per complex multiply-add.
+__device__ __forceinline__ void cmac2(float2& acc, float a, float b, float2 B, float2 Bp) {
+  acc = __ffma2_rn(make_float2(a, a), B, acc);
+  acc = __ffma2_rn(make_float2(b, b), Bp, acc);
 }
 
 // compile-time loop: f(integral_constant<int, i>) for i = B, B+S, ... (excluding E)
@@ -58,17 +60,24 @@ __device__ __forceinline__ void sfor(F&& f) {
   }
 }
 
+// Is holds, per (j, mp): Is[2 ci] = (Re I, Im I, -Im I, Re I) of I_j^mp and
+// Is[2 ci + 1] the same for I_j^{-mp} = (-1)^mp conj(I_j^mp).  For a complex
+// M = (ar, ai):  M * I = ar (Re I, Im I) + ai (-Im I, Re I).
 template <int P>
-__device__ __forceinline__ void m2l_accumulate(const float2* __restrict__ Is, const float (&Mr)[Dims<P>::NC],
-                                               const float (&Mi)[Dims<P>::NC], float (&Lr)[Dims<P>::NC],
-                                               float (&Li)[Dims<P>::NC]) {
+__device__ __forceinline__ void m2l_accumulate(const float4* __restrict__ Is, const float (&Mr)[Dims<P>::NC],
+                                               const float (&Mi)[Dims<P>::NC], float2 (&L)[Dims<P>::NC]) {
   sfor<P - 1, -1, -1>([&](auto J) {                // I degree j = n + k, high -> low
     constexpr int j = decltype(J)::value;
     sfor<j, -1, -1>([&](auto MPc) {
       constexpr int mp = decltype(MPc)::value;
-      const float2 iv = Is[ci(j, mp)];
-      const float ir = iv.x, ii = iv.y;
-      constexpr float ts = (mp & 1) ? -1.f : 1.f;  // I_j^{-mp} = ts conj(I_j^mp)
+      const float4 ip = Is[2 * ci(j, mp)];
+      const float2 Bp = make_float2(ip.x, ip.y), Bq = make_float2(ip.z, ip.w);
+      float2 Cp = Bp, Cq = Bq;
+      if constexpr (mp > 0) {
+        const float4 in = Is[2 * ci(j, mp) + 1];
+        Cp = make_float2(in.x, in.y);
+        Cq = make_float2(in.z, in.w);
+      }
       sfor<0, j + 1, 1>([&](auto Nc) {
         constexpr int n = decltype(Nc)::value;
         constexpr int k = j - n;
@@ -78,21 +87,52 @@ __device__ __forceinline__ void m2l_accumulate(const float2* __restrict__ Is, co
           constexpr int m1 = mp - l;               // term with I_j^{+mp}
           if constexpr (m1 >= -n && m1 <= n) {
             if constexpr (m1 >= 0) {
-              cmac(Lr[o], Li[o], Mr[ci(n, m1)], Mi[ci(n, m1)], ir, ii);
+              cmac2(L[o], Mr[ci(n, m1)], Mi[ci(n, m1)], Bp, Bq);
             } else {
               constexpr float s = ((-m1) & 1) ? -1.f : 1.f;   // M_n^m = s conj(M_n^{-m})
-              cmac(Lr[o], Li[o], s * Mr[ci(n, -m1)], -s * Mi[ci(n, -m1)], ir, ii);
+              cmac2(L[o], s * Mr[ci(n, -m1)], -s * Mi[ci(n, -m1)], Bp, Bq);
             }
           }
           constexpr int m2 = -mp - l;              // term with I_j^{-mp}
           if constexpr (mp > 0 && m2 >= -n) {
             constexpr float s = ((-m2) & 1) ? -1.f : 1.f;
-            cmac(Lr[o], Li[o], s * Mr[ci(n, -m2)], -s * Mi[ci(n, -m2)], ts * ir, -ts * ii);
+            cmac2(L[o], s * Mr[ci(n, -m2)], -s * Mi[ci(n, -m2)], Cp, Cq);
           }
         });
       });
     });
   });
+}
+
+// column m of I_j^m(D), j = m .. P-1, written in the expanded layout above
+template <int P>
+__device__ void irregular_column_x(float x, float y, float z, int m, float4* __restrict__ Is) {
+  const float r2 = x * x + y * y + z * z;
+  const float ir2 = 1.0f / r2;
+  float dr = rsqrtf(r2), di = 0.f;
+  for (int i = 1; i <= m; ++i) {
+    const float s = -(float)(2 * i - 1) * ir2;
+    const float nr = s * (x * dr - y * di), ni = s * (x * di + y * dr);
+    dr = nr;
+    di = ni;
+  }
+  const float ts = (m & 1) ? -1.f : 1.f;
+  auto put = [&](int n, float vr, float vi) {
+    Is[2 * ci(n, m)] = make_float4(vr, vi, -vi, vr);
+    Is[2 * ci(n, m) + 1] = make_float4(ts * vr, -ts * vi, ts * vi, ts * vr);
+  };
+  put(m, dr, di);
+  if (m + 1 >= P) return;
+  float ar = (float)(2 * m + 1) * z * ir2 * dr, ai = (float)(2 * m + 1) * z * ir2 * di;
+  put(m + 1, ar, ai);
+  float br = dr, bi = di;
+  for (int n = m + 2; n < P; ++n) {
+    const float c1 = (float)(2 * n - 1) * z, c2 = (float)(n - 1 - m) * (float)(n - 1 + m);
+    const float vr = (c1 * ar - c2 * br) * ir2, vi = (c1 * ai - c2 * bi) * ir2;
+    put(n, vr, vi);
+    br = ar; bi = ai;
+    ar = vr; ai = vi;
+  }
 }
 
 template <int P>
@@ -101,7 +141,7 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
                                                 const float2* __restrict__ M, float2* __restrict__ Lc) {
   using D = Dims<P>;
   constexpr int NC = D::NC, P2 = D::P2, S = D::S;
-  extern __shared__ float2 sm[];                   // [kSub][S] harmonics, later the reduction buffer
+  extern __shared__ float4 sm4[];                  // [kSub][S] harmonics, later the reduction buffer
   __shared__ float4 Dsh[kSub];
   const int t = blockIdx.x;
   const int b = seg_b[t], e = seg_e[t];
@@ -115,9 +155,9 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
   const long long ctz = (long long)(2 * c.qz[t] + 1) << (kMaxLevel - lt);
   const float inv_st = ldexpf(1.0f, -(kMaxLevel + 1 - lt));
 
-  float Lr[NC], Li[NC];
+  float2 L[NC];
 #pragma unroll
-  for (int o = 0; o < NC; ++o) { Lr[o] = 0.f; Li[o] = 0.f; }
+  for (int o = 0; o < NC; ++o) L[o] = make_float2(0.f, 0.f);
 
 #pragma unroll 1
   for (int q0 = b; q0 < e; q0 += kSub) {
@@ -143,7 +183,7 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
     for (int task = lane; task < kSub * P2; task += 32) {
       const int s = task / P2, m = task - P2 * (task / P2);
       const float4 dv = Dsh[s];
-      irregular_column<float>(dv.x, dv.y, dv.z, m, P2, (cpx<float>*)(sm + s * S));
+      irregular_column_x<P>(dv.x, dv.y, dv.z, m, sm4 + s * S);
     }
     // this lane's source multipole component, scaled by (s_s/s_t)^n
     float Mr[NC], Mi[NC];
@@ -170,15 +210,15 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
       }
     }
     __syncwarp();
-    m2l_accumulate<P>(sm + (act ? sub : 0) * S, Mr, Mi, Lr, Li);
+    m2l_accumulate<P>(sm4 + (act ? sub : 0) * S, Mr, Mi, L);
     __syncwarp();
   }
 
   // deterministic reduction over the source subsets
-  float2* red = sm;                                // [kSub][3][NC]
+  float2* red = (float2*)sm4;                      // [kSub][3][NC]
   if (act) {
 #pragma unroll
-    for (int o = 0; o < NC; ++o) red[(sub * 3 + comp) * NC + o] = make_float2(Lr[o], Li[o]);
+    for (int o = 0; o < NC; ++o) red[(sub * 3 + comp) * NC + o] = L[o];
   }
   __syncwarp();
   for (int i = lane; i < 3 * NC; i += 32) {
@@ -201,7 +241,7 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
 template <int P>
 void launch_reg(Ctx& c) {
   using D = Dims<P>;
-  size_t sm = sizeof(float2) * (size_t)kSub * D::S;
+  size_t sm = sizeof(float4) * (size_t)kSub * D::S;
   size_t red = sizeof(float2) * (size_t)kSub * 3 * D::NC;
   if (red > sm) sm = red;
   MCells mc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p};

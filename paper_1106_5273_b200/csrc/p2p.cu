@@ -7,105 +7,233 @@
 // (readings Z1, Z3, Z4, Z7).  sum_j f (alpha_j x alpha_i) is
 // accumulated as (sum_j f alpha_j) x alpha_i.
 //
-// Mapping: one thread block per target leaf, one target particle per thread
-// held in registers; each source leaf of the target's segment is staged in
-// shared memory as float4 tiles in *target-leaf-centred* coordinates -- the
-// image shift and the centring are done once per source in double and rounded
-// to FP32 ("Fix B") -- and the FP32 partial over each tile
-// (<= 64 sources) is added to a per-target FP64 accumulator ("Fix A").
+// Mapping (sm_100a, FP32-issue bound): one warp per target leaf, two target
+// particles per lane held in registers, so every shared-memory source load
+// feeds two pair evaluations.  Each source leaf of the target's segment is
+// staged in shared memory as float4 tiles in *target-leaf-centred*
+// coordinates -- the image shift and the centring are done once per source in
+// double and rounded to FP32 ("Fix B") -- and the FP32
+// partial over each tile (<= 64 sources) is added to a per-target FP64
+// accumulator ("Fix A").  MUFU ops are the approximate .ftz forms.
+//
+// Cutoff g (Eq. 2).  Table 1 counts two expf and no erf, i.e. the
+// paper's kernel approximated erf (reading Z6).  Here g is evaluated without
+// erf: a 9-term Taylor series of g/rho^3 in rho^2 for rho < 0.8, and
+// g = 1 - e^{-rho^2} (erfcx(rho) + (2/sqrt pi) rho) with erfcx fitted by a
+// degree-6 polynomial in t = 1/(1 + rho/2) above; |g - g_exact| <= 2e-7 (FP32
+// evaluation, checked by the parity tests through fmm_eval_cutoff).  Source
+// tiles whose every pair has rho >= 4.5 (checked per tile from the leaf
+// boxes and the tile's largest sigma) take the exact singular branch: there
+// 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
 #include "ctx.cuh"
 
 namespace fmmb {
 
 namespace {
 
-constexpr int TP = 64;
+constexpr int TP = 64;           // targets per block pass and sources per tile
+constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// g(rho) of Eq. 2 given rho, x = rho^2 and e = exp(-rho^2) (see header).
+__device__ __forceinline__ float cutoff_g(float rho, float x, float e) {
+  float s = 2.945851975e-06f;
+  s = fmaf(s, x, -2.633938311e-05f);
+  s = fmaf(s, x, 2.089590998e-04f);
+  s = fmaf(s, x, -1.446640003e-03f);
+  s = fmaf(s, x, 8.548326790e-03f);
+  s = fmaf(s, x, -4.179182276e-02f);
+  s = fmaf(s, x, 1.611970216e-01f);
+  s = fmaf(s, x, -4.513516724e-01f);
+  s = fmaf(s, x, 7.522527575e-01f);
+  const float gs = s * (rho * x);
+  const float t = rcp_approx(fmaf(0.5f, rho, 1.0f));
+  float h = 6.501056254e-02f;
+  h = fmaf(h, t, -4.661040902e-01f);
+  h = fmaf(h, t, 9.906343818e-01f);
+  h = fmaf(h, t, -3.476467133e-01f);
+  h = fmaf(h, t, 5.238698721e-01f);
+  h = fmaf(h, t, 2.293880880e-01f);
+  h = fmaf(h, t, 4.825282376e-03f);
+  const float gl = fmaf(-e, fmaf(1.1283791670955126f, rho, h), 1.0f);
+  return x < 0.64f ? gs : gl;
+}
 
 struct PCells {
   const int *level, *qx, *qy, *qz, *begin, *count;
 };
 
-__global__ void __launch_bounds__(TP) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
+struct Acc {
+  float u0, u1, u2, s0, s1, s2, a0, a1, a2;
+};
+
+__device__ __forceinline__ void zero(Acc& a) { a.u0 = a.u1 = a.u2 = a.s0 = a.s1 = a.s2 = a.a0 = a.a1 = a.a2 = 0.f; }
+
+// one pair; NEAR selects the regularised kernel, else the singular one
+template <bool NEAR>
+__device__ __forceinline__ void pair(Acc& A, float xi0, float xi1, float xi2, float ai0, float ai1, float ai2,
+                                     const float4 q, const float4 a) {
+  const float rx = xi0 - q.x, ry = xi1 - q.y, rz = xi2 - q.z;
+  const float r2 = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+  const float inv = rsqrt_approx(fmaxf(r2, 1e-12f));   // r = 0 => g = 0 below (Z7)
+  const float inv2 = inv * inv;
+  const float inv3 = inv2 * inv;
+  float f, fp;
+  if (NEAR) {
+    const float x = -r2 * q.w;                      // q.w = -1/(2 sigma^2) => x = rho^2
+    const float e = ex2_approx(x * -1.4426950408889634f);
+    const float rho = r2 * inv * a.w;               // a.w = 1/(sqrt2 sigma)
+    const float g = cutoff_g(rho, x, e);
+    f = g * inv3;
+    fp = fmaf(2.2567583341910252f * rho * x, e, -3.0f * g) * (inv3 * inv2);
+  } else {
+    f = inv3;
+    fp = -3.0f * inv3 * inv2;
+  }
+  const float c0 = fmaf(a.y, rz, -a.z * ry), c1 = fmaf(a.z, rx, -a.x * rz), c2 = fmaf(a.x, ry, -a.y * rx);
+  A.u0 = fmaf(f, c0, A.u0); A.u1 = fmaf(f, c1, A.u1); A.u2 = fmaf(f, c2, A.u2);
+  A.a0 = fmaf(f, a.x, A.a0); A.a1 = fmaf(f, a.y, A.a1); A.a2 = fmaf(f, a.z, A.a2);
+  const float qq = fp * fmaf(rz, ai2, fmaf(ry, ai1, rx * ai0));
+  A.s0 = fmaf(qq, c0, A.s0); A.s1 = fmaf(qq, c1, A.s1); A.s2 = fmaf(qq, c2, A.s2);
+}
+
+struct DAcc {
+  double u0, u1, u2, s0, s1, s2, a0, a1, a2;
+};
+
+__device__ __forceinline__ void flush(DAcc& D, const Acc& A) {
+  D.u0 += A.u0; D.u1 += A.u1; D.u2 += A.u2;
+  D.s0 += A.s0; D.s1 += A.s1; D.s2 += A.s2;
+  D.a0 += A.a0; D.a1 += A.a1; D.a2 += A.a2;
+}
+
+__global__ void __launch_bounds__(NT) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             const float4* __restrict__ pos, const float4* __restrict__ alp,
                                             float* __restrict__ un, float* __restrict__ sn) {
-  __shared__ float4 sx[TP];   // (x', y', z', 1/(2 sigma^2))
+  __shared__ float4 sx[TP];   // (x', y', z', -1/(2 sigma^2))
   __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
   const float k4 = (float)(1.0 / (4.0 * kPi));
-  int leaf = leaf_ids[blockIdx.x];
-  int lev = c.level[leaf], tb = c.begin[leaf], tcnt = c.count[leaf];
-  double s = L / (double)(1 << lev);
-  double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s, cz = lo2 + (c.qz[leaf] + 0.5) * s;
-  int eb = seg_b[leaf], ee = seg_e[leaf];
+  const int lane = threadIdx.x;
+  const int leaf = leaf_ids[blockIdx.x];
+  const int lev = c.level[leaf], tb = c.begin[leaf], tcnt = c.count[leaf];
+  const double s = L / (double)(1 << lev);
+  const double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s,
+               cz = lo2 + (c.qz[leaf] + 0.5) * s;
+  const int eb = seg_b[leaf], ee = seg_e[leaf];
   for (int t0 = 0; t0 < tcnt; t0 += TP) {
-    int i = t0 + threadIdx.x;
-    bool valid = i < tcnt;
-    float xi0 = 0.f, xi1 = 0.f, xi2 = 0.f;
-    float4 ai = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) {
-      float4 p = pos[tb + i];
-      xi0 = (float)((double)p.x - cx);
-      xi1 = (float)((double)p.y - cy);
-      xi2 = (float)((double)p.z - cz);
-      ai = alp[tb + i];
+    const int i0 = t0 + lane, i1 = t0 + lane + NT;
+    const bool v0 = i0 < tcnt, v1 = i1 < tcnt;
+    float x00 = 0.f, x01 = 0.f, x02 = 0.f, x10 = 0.f, x11 = 0.f, x12 = 0.f;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (v0) {
+      const float4 p = pos[tb + i0];
+      x00 = (float)((double)p.x - cx); x01 = (float)((double)p.y - cy); x02 = (float)((double)p.z - cz);
+      a0 = alp[tb + i0];
     }
-    double du0 = 0, du1 = 0, du2 = 0, ds0 = 0, ds1 = 0, ds2 = 0, dA0 = 0, dA1 = 0, dA2 = 0;
+    if (v1) {
+      const float4 p = pos[tb + i1];
+      x10 = (float)((double)p.x - cx); x11 = (float)((double)p.y - cy); x12 = (float)((double)p.z - cz);
+      a1 = alp[tb + i1];
+    }
+    DAcc D0 = {0, 0, 0, 0, 0, 0, 0, 0, 0}, D1 = D0;
     for (int e = eb; e < ee; ++e) {
-      uint64_t ent = lst[e];
-      int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
-      double shx = (img % 3 - 1) * L - cx, shy = ((img / 3) % 3 - 1) * L - cy, shz = (img / 9 - 1) * L - cz;
-      int sb = c.begin[src], scnt = c.count[src];
+      const uint64_t ent = lst[e];
+      const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
+      const int ls = c.level[src];
+      const double ss = L / (double)(1 << ls);
+      // source box centre relative to the target leaf centre, image included
+      const double ox = (c.qx[src] + 0.5) * ss + lo0 + (img % 3 - 1) * L - cx;
+      const double oy = (c.qy[src] + 0.5) * ss + lo1 + ((img / 3) % 3 - 1) * L - cy;
+      const double oz = (c.qz[src] + 0.5) * ss + lo2 + (img / 9 - 1) * L - cz;
+      const double shx = (img % 3 - 1) * L - cx, shy = ((img / 3) % 3 - 1) * L - cy, shz = (img / 9 - 1) * L - cz;
+      // minimum distance between the two leaf cubes
+      const double hsum = 0.5 * (s + ss);
+      const double gx = fmax(0.0, fabs(ox) - hsum), gy = fmax(0.0, fabs(oy) - hsum), gz = fmax(0.0, fabs(oz) - hsum);
+      const float dmin2 = (float)(gx * gx + gy * gy + gz * gz);
+      const int sb = c.begin[src], scnt = c.count[src];
       for (int s0 = 0; s0 < scnt; s0 += TP) {
-        __syncthreads();
-        int j = s0 + threadIdx.x;
-        if (j < scnt) {
-          float4 p = pos[sb + j];
-          float4 a = alp[sb + j];
-          float kk = 1.0f / (2.0f * p.w * p.w);
-          sx[threadIdx.x] = make_float4((float)((double)p.x + shx), (float)((double)p.y + shy),
-                                        (float)((double)p.z + shz), kk);
-          sa[threadIdx.x] = make_float4(a.x * k4, a.y * k4, a.z * k4, sqrtf(kk));
-        }
-        __syncthreads();
-        int nj = min(TP, scnt - s0);
-        if (valid) {
-          float pu0 = 0.f, pu1 = 0.f, pu2 = 0.f, ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, pA0 = 0.f, pA1 = 0.f, pA2 = 0.f;
-          for (int jj = 0; jj < nj; ++jj) {
-            float4 q = sx[jj];
-            float4 a = sa[jj];
-            float rx = xi0 - q.x, ry = xi1 - q.y, rz = xi2 - q.z;
-            float r2 = rx * rx + ry * ry + rz * rz;
-            float inv = r2 > 0.f ? rsqrtf(r2) : 0.f;
-            float rho2 = r2 * q.w;
-            float rho = r2 * inv * a.w;
-            float ex = __expf(-rho2);
-            float g = erff(rho) - 1.1283791670955126f * rho * ex;
-            float inv2 = inv * inv;
-            float inv3 = inv2 * inv;
-            float f = g * inv3;
-            float fp = (2.2567583341910252f * rho * rho2 * ex - 3.0f * g) * inv3 * inv2;
-            float c0 = a.y * rz - a.z * ry, c1 = a.z * rx - a.x * rz, c2 = a.x * ry - a.y * rx;
-            pu0 += f * c0; pu1 += f * c1; pu2 += f * c2;
-            pA0 += f * a.x; pA1 += f * a.y; pA2 += f * a.z;
-            float qq = fp * (rx * ai.x + ry * ai.y + rz * ai.z);
-            ps0 += qq * c0; ps1 += qq * c1; ps2 += qq * c2;
+        __syncwarp();
+        float smax = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = s0 + lane + h * NT;
+          if (j < scnt) {
+            const float4 p = pos[sb + j];
+            const float4 a = alp[sb + j];
+            const float w = 1.0f / (2.0f * p.w * p.w);
+            sx[lane + h * NT] = make_float4((float)((double)p.x + shx), (float)((double)p.y + shy),
+                                            (float)((double)p.z + shz), -w);
+            sa[lane + h * NT] = make_float4(a.x * k4, a.y * k4, a.z * k4, sqrtf(w));
+            smax = fmaxf(smax, p.w);
           }
-          du0 += pu0; du1 += pu1; du2 += pu2;
-          ds0 += ps0; ds1 += ps1; ds2 += ps2;
-          dA0 += pA0; dA1 += pA1; dA2 += pA2;
         }
+        for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        __syncwarp();
+        const int nj = min(TP, scnt - s0);
+        // every pair of this tile has rho >= 4.5 => exact singular branch
+        const bool far = dmin2 >= 40.5f * smax * smax;
+        Acc A0, A1;
+        zero(A0);
+        zero(A1);
+        if (far) {
+#pragma unroll 4
+          for (int jj = 0; jj < nj; ++jj) {
+            const float4 q = sx[jj], a = sa[jj];
+            pair<false>(A0, x00, x01, x02, a0.x, a0.y, a0.z, q, a);
+            pair<false>(A1, x10, x11, x12, a1.x, a1.y, a1.z, q, a);
+          }
+        } else {
+#pragma unroll 2
+          for (int jj = 0; jj < nj; ++jj) {
+            const float4 q = sx[jj], a = sa[jj];
+            pair<true>(A0, x00, x01, x02, a0.x, a0.y, a0.z, q, a);
+            pair<true>(A1, x10, x11, x12, a1.x, a1.y, a1.z, q, a);
+          }
+        }
+        flush(D0, A0);
+        flush(D1, A1);
       }
     }
-    if (valid) {
-      // (sum_j f alpha_j) x alpha_i
-      ds0 += dA1 * ai.z - dA2 * ai.y;
-      ds1 += dA2 * ai.x - dA0 * ai.z;
-      ds2 += dA0 * ai.y - dA1 * ai.x;
-      int64_t o = 3 * (int64_t)(tb + i);
-      un[o] = (float)du0; un[o + 1] = (float)du1; un[o + 2] = (float)du2;
-      sn[o] = (float)ds0; sn[o + 1] = (float)ds1; sn[o + 2] = (float)ds2;
+    // s += (sum_j f alpha_j) x alpha_i
+    if (v0) {
+      const int64_t o = 3 * (int64_t)(tb + i0);
+      un[o] = (float)D0.u0; un[o + 1] = (float)D0.u1; un[o + 2] = (float)D0.u2;
+      sn[o] = (float)(D0.s0 + (D0.a1 * a0.z - D0.a2 * a0.y));
+      sn[o + 1] = (float)(D0.s1 + (D0.a2 * a0.x - D0.a0 * a0.z));
+      sn[o + 2] = (float)(D0.s2 + (D0.a0 * a0.y - D0.a1 * a0.x));
     }
+    if (v1) {
+      const int64_t o = 3 * (int64_t)(tb + i1);
+      un[o] = (float)D1.u0; un[o + 1] = (float)D1.u1; un[o + 2] = (float)D1.u2;
+      sn[o] = (float)(D1.s0 + (D1.a1 * a1.z - D1.a2 * a1.y));
+      sn[o + 1] = (float)(D1.s1 + (D1.a2 * a1.x - D1.a0 * a1.z));
+      sn[o + 2] = (float)(D1.s2 + (D1.a0 * a1.y - D1.a1 * a1.x));
+    }
+  }
+}
+
+__global__ void k_eval_cutoff(const float* __restrict__ rho, int64_t n, float* __restrict__ g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float r = rho[i];
+    const float x = r * r;
+    g[i] = cutoff_g(r, x, ex2_approx(x * -1.4426950408889634f));
   }
 }
 
@@ -114,9 +242,12 @@ __global__ void __launch_bounds__(TP) k_p2p(const int* __restrict__ leaf_ids, co
 void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   if (c.nleaves == 0) return;
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
-  FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, TP, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
-                                                  c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near);
-  FMM_LAUNCH_CHECK();
+  FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
+             c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near);
+}
+
+void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {
+  FMM_LAUNCH(c, k_eval_cutoff, nblocks(n, 256), 256, 0, rho, n, g);
 }
 
 }  // namespace fmmb

@@ -74,9 +74,10 @@ def lib():
         L.fmm_get_cells.argtypes = [vp, vp]
         L.fmm_get_lists.argtypes = [vp, vp, vp]
         L.fmm_get_expansions.argtypes = [vp, vp, vp]
+        L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
-                   "fmm_get_lists", "fmm_get_expansions"):
+                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
@@ -194,6 +195,10 @@ def fmm_get_expansions(ctx, order):
     L = np.zeros((nc, 3, k, 2), dtype=np.float32)
     _check(ctx, lib().fmm_get_expansions(ctx, C.c_void_p(M.ctypes.data), C.c_void_p(L.ctypes.data)))
     return (M[..., 0] + 1j * M[..., 1]).astype(np.complex128), (L[..., 0] + 1j * L[..., 1]).astype(np.complex128)
+
+
+def fmm_eval_cutoff(ctx, rho, g):
+    _check(ctx, lib().fmm_eval_cutoff(ctx, int(rho.shape[0]), _ptr(rho), _ptr(g)))
 
 
 class FMM:

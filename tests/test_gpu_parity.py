@@ -207,3 +207,20 @@ def test_c3_tg256_closed_form_full_size(oracle_mod):
     uc, sc = _tg_closed_form(x.astype(np.float64), a.astype(np.float64), float(s[0]))
     assert oracle_mod.rel_l2(u, uc) <= 1e-3 and oracle_mod.rel_l2(st, sc) <= 1e-3
     g.close()
+
+
+def test_device_cutoff_within_reading_z6():
+    """The FP32 cutoff the P2P kernel uses meets reading Z6: |g - g_exact| <= 2e-7
+    on a dense rho grid (g_exact from scipy's erf, Eq. 2)."""
+    import paper_1106_5273_b200 as P
+    from scipy.special import erf
+    rho = np.linspace(0, 12, 1_200_001).astype(np.float32)
+    g = np.zeros_like(rho)
+    f = P.FMM(images=3)
+    P.fmm_eval_cutoff(f.ctx, rho, g)
+    r = rho.astype(np.float64)
+    gx = erf(r) - 2 / np.sqrt(np.pi) * r * np.exp(-r * r)
+    assert np.max(np.abs(g - gx)) <= 2e-7
+    nz = r > 0.05
+    assert np.max(np.abs(g[nz] - gx[nz]) / gx[nz]) <= 5e-6
+    f.close()
