@@ -18,10 +18,13 @@
 //
 // Cutoff g (Eq. 2).  Table 1 counts two expf and no erf, i.e. the
 // paper's kernel approximated erf (reading Z6).  Here g is evaluated without
-// erf: a 9-term Taylor series of g/rho^3 in rho^2 for rho < 0.8, and
-// g = 1 - e^{-rho^2} (erfcx(rho) + (2/sqrt pi) rho) with erfcx fitted by a
-// degree-6 polynomial in t = 1/(1 + rho/2) above; |g - g_exact| <= 2e-7 (FP32
-// evaluation, checked by the parity tests through fmm_eval_cutoff).  Source
+// erf: g = 1 - e^{-rho^2} (erfcx(rho) + (2/sqrt pi) rho) with erfcx fitted by a
+// degree-6 polynomial in t = 1/(1 + rho/2), and a 9-term Taylor series of
+// g/rho^3 in rho^2 for rho < 0.8 (evaluated only when some lane of the warp
+// has such a close pair); |g - g_exact| <= 2e-7 (FP32 evaluation, checked by
+// the parity tests through fmm_eval_cutoff).  The pair arithmetic of the two
+// targets of a lane is packed into FP32x2 (FFMA2) with the source operands
+// broadcast, halving the issue slots per pair.  Source
 // tiles whose every pair has rho >= 4.5 (checked per tile from the leaf
 // boxes and the tile's largest sigma) take the exact singular branch: there
 // 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
@@ -50,79 +53,101 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// g(rho) of Eq. 2 given rho, x = rho^2 and e = exp(-rho^2) (see header).
+// g(rho) of Eq. 2 from rho, x = rho^2, e = exp(-rho^2): the two pieces.
+//   series: g = rho^3 sum_k a_k x^k               (accurate as rho -> 0; used for x < 0.64)
+//   erfcx : g = 1 - e (h(t) + (2/sqrt pi) rho),  h ~ erfcx, t = 1/(1 + rho/2)
+__device__ __forceinline__ float2 series_g(float2 rho, float2 x) {
+  float2 s = make_float2(2.945851975e-06f, 2.945851975e-06f);
+  const float a[8] = {-2.633938311e-05f, 2.089590998e-04f, -1.446640003e-03f, 8.548326790e-03f,
+                      -4.179182276e-02f, 1.611970216e-01f, -4.513516724e-01f, 7.522527575e-01f};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s = __ffma2_rn(s, x, make_float2(a[k], a[k]));
+  return __fmul2_rn(s, __fmul2_rn(rho, x));
+}
+__device__ __forceinline__ float2 erfcx_g(float2 rho, float2 e) {
+  const float2 d = __ffma2_rn(make_float2(0.5f, 0.5f), rho, make_float2(1.f, 1.f));
+  const float2 t = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+  float2 h = make_float2(6.501056254e-02f, 6.501056254e-02f);
+  const float c[6] = {-4.661040902e-01f, 9.906343818e-01f, -3.476467133e-01f, 5.238698721e-01f,
+                      2.293880880e-01f, 4.825282376e-03f};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) h = __ffma2_rn(h, t, make_float2(c[k], c[k]));
+  const float2 y = __ffma2_rn(make_float2(1.1283791670955126f, 1.1283791670955126f), rho, h);
+  return __ffma2_rn(make_float2(-e.x, -e.y), y, make_float2(1.f, 1.f));
+}
+// scalar form (same arithmetic) for fmm_eval_cutoff
 __device__ __forceinline__ float cutoff_g(float rho, float x, float e) {
-  float s = 2.945851975e-06f;
-  s = fmaf(s, x, -2.633938311e-05f);
-  s = fmaf(s, x, 2.089590998e-04f);
-  s = fmaf(s, x, -1.446640003e-03f);
-  s = fmaf(s, x, 8.548326790e-03f);
-  s = fmaf(s, x, -4.179182276e-02f);
-  s = fmaf(s, x, 1.611970216e-01f);
-  s = fmaf(s, x, -4.513516724e-01f);
-  s = fmaf(s, x, 7.522527575e-01f);
-  const float gs = s * (rho * x);
-  const float t = rcp_approx(fmaf(0.5f, rho, 1.0f));
-  float h = 6.501056254e-02f;
-  h = fmaf(h, t, -4.661040902e-01f);
-  h = fmaf(h, t, 9.906343818e-01f);
-  h = fmaf(h, t, -3.476467133e-01f);
-  h = fmaf(h, t, 5.238698721e-01f);
-  h = fmaf(h, t, 2.293880880e-01f);
-  h = fmaf(h, t, 4.825282376e-03f);
-  const float gl = fmaf(-e, fmaf(1.1283791670955126f, rho, h), 1.0f);
-  return x < 0.64f ? gs : gl;
+  const float2 gs = series_g(make_float2(rho, rho), make_float2(x, x));
+  const float2 gl = erfcx_g(make_float2(rho, rho), make_float2(e, e));
+  return x < 0.64f ? gs.x : gl.x;
 }
 
 struct PCells {
   const int *level, *qx, *qy, *qz, *begin, *count;
 };
 
-struct Acc {
-  float u0, u1, u2, s0, s1, s2, a0, a1, a2;
+// accumulators of the two targets of a lane, packed (target 0, target 1)
+struct Acc2 {
+  float2 u0, u1, u2, s0, s1, s2, a0, a1, a2;
 };
+__device__ __forceinline__ void zero(Acc2& A) {
+  A.u0 = A.u1 = A.u2 = A.s0 = A.s1 = A.s2 = A.a0 = A.a1 = A.a2 = make_float2(0.f, 0.f);
+}
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-__device__ __forceinline__ void zero(Acc& a) { a.u0 = a.u1 = a.u2 = a.s0 = a.s1 = a.s2 = a.a0 = a.a1 = a.a2 = 0.f; }
-
-// one pair; NEAR selects the regularised kernel, else the singular one
+// one source (q: position, -1/(2 sigma^2); a: alpha/(4 pi), 1/(sqrt2 sigma)) on
+// the lane's two targets, all arithmetic packed FP32x2 (FFMA2/FMUL2/FADD2).
+// NEAR selects the regularised kernel, else the exact singular one.
 template <bool NEAR>
-__device__ __forceinline__ void pair(Acc& A, float xi0, float xi1, float xi2, float ai0, float ai1, float ai2,
-                                     const float4 q, const float4 a) {
-  const float rx = xi0 - q.x, ry = xi1 - q.y, rz = xi2 - q.z;
-  const float r2 = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
-  const float inv = rsqrt_approx(fmaxf(r2, 1e-12f));   // r = 0 => g = 0 below (Z7)
-  const float inv2 = inv * inv;
-  const float inv3 = inv2 * inv;
-  float f, fp;
+__device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, float2 b0, float2 b1, float2 b2,
+                                      const float4 q, const float4 a) {
+  const float2 rx = __fadd2_rn(x0, bc(-q.x)), ry = __fadd2_rn(x1, bc(-q.y)), rz = __fadd2_rn(x2, bc(-q.z));
+  const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
+  const float2 inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
+  const float2 inv2 = __fmul2_rn(inv, inv);
+  const float2 inv3 = __fmul2_rn(inv2, inv);
+  float2 f, fp;
   if (NEAR) {
-    const float x = -r2 * q.w;                      // q.w = -1/(2 sigma^2) => x = rho^2
-    const float e = ex2_approx(x * -1.4426950408889634f);
-    const float rho = r2 * inv * a.w;               // a.w = 1/(sqrt2 sigma)
-    const float g = cutoff_g(rho, x, e);
-    f = g * inv3;
-    fp = fmaf(2.2567583341910252f * rho * x, e, -3.0f * g) * (inv3 * inv2);
+    const float2 x = __fmul2_rn(r2, bc(-q.w));                 // rho^2
+    const float2 ea = __fmul2_rn(x, bc(-1.4426950408889634f));
+    const float2 e = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
+    const float2 rho = __fmul2_rn(__fmul2_rn(r2, inv), bc(a.w));
+    float2 g = erfcx_g(rho, e);
+    // series piece only when some lane has a close pair (warp-uniform branch)
+    if (__any_sync(0xffffffffu, fminf(x.x, x.y) < 0.64f)) {
+      const float2 gs = series_g(rho, x);
+      g = make_float2(x.x < 0.64f ? gs.x : g.x, x.y < 0.64f ? gs.y : g.y);
+    }
+    f = __fmul2_rn(g, inv3);
+    const float2 t1 = __fmul2_rn(__fmul2_rn(rho, x), bc(2.2567583341910252f));   // (4/sqrt pi) rho^3
+    fp = __fmul2_rn(__ffma2_rn(t1, e, __fmul2_rn(g, bc(-3.0f))), __fmul2_rn(inv3, inv2));
   } else {
     f = inv3;
-    fp = -3.0f * inv3 * inv2;
+    fp = __fmul2_rn(__fmul2_rn(inv3, inv2), bc(-3.0f));
   }
-  const float c0 = fmaf(a.y, rz, -a.z * ry), c1 = fmaf(a.z, rx, -a.x * rz), c2 = fmaf(a.x, ry, -a.y * rx);
-  A.u0 = fmaf(f, c0, A.u0); A.u1 = fmaf(f, c1, A.u1); A.u2 = fmaf(f, c2, A.u2);
-  A.a0 = fmaf(f, a.x, A.a0); A.a1 = fmaf(f, a.y, A.a1); A.a2 = fmaf(f, a.z, A.a2);
-  const float qq = fp * fmaf(rz, ai2, fmaf(ry, ai1, rx * ai0));
-  A.s0 = fmaf(qq, c0, A.s0); A.s1 = fmaf(qq, c1, A.s1); A.s2 = fmaf(qq, c2, A.s2);
+  const float2 c0 = __ffma2_rn(bc(a.y), rz, __fmul2_rn(bc(-a.z), ry));
+  const float2 c1 = __ffma2_rn(bc(a.z), rx, __fmul2_rn(bc(-a.x), rz));
+  const float2 c2 = __ffma2_rn(bc(a.x), ry, __fmul2_rn(bc(-a.y), rx));
+  A.u0 = __ffma2_rn(f, c0, A.u0); A.u1 = __ffma2_rn(f, c1, A.u1); A.u2 = __ffma2_rn(f, c2, A.u2);
+  A.a0 = __ffma2_rn(f, bc(a.x), A.a0); A.a1 = __ffma2_rn(f, bc(a.y), A.a1); A.a2 = __ffma2_rn(f, bc(a.z), A.a2);
+  const float2 qq = __fmul2_rn(fp, __ffma2_rn(rz, b2, __ffma2_rn(ry, b1, __fmul2_rn(rx, b0))));
+  A.s0 = __ffma2_rn(qq, c0, A.s0); A.s1 = __ffma2_rn(qq, c1, A.s1); A.s2 = __ffma2_rn(qq, c2, A.s2);
 }
 
 struct DAcc {
   double u0, u1, u2, s0, s1, s2, a0, a1, a2;
 };
 
-__device__ __forceinline__ void flush(DAcc& D, const Acc& A) {
-  D.u0 += A.u0; D.u1 += A.u1; D.u2 += A.u2;
-  D.s0 += A.s0; D.s1 += A.s1; D.s2 += A.s2;
-  D.a0 += A.a0; D.a1 += A.a1; D.a2 += A.a2;
+__device__ __forceinline__ void flush(DAcc& D0, DAcc& D1, const Acc2& A) {
+  D0.u0 += A.u0.x; D0.u1 += A.u1.x; D0.u2 += A.u2.x;
+  D0.s0 += A.s0.x; D0.s1 += A.s1.x; D0.s2 += A.s2.x;
+  D0.a0 += A.a0.x; D0.a1 += A.a1.x; D0.a2 += A.a2.x;
+  D1.u0 += A.u0.y; D1.u1 += A.u1.y; D1.u2 += A.u2.y;
+  D1.s0 += A.s0.y; D1.s1 += A.s1.y; D1.s2 += A.s2.y;
+  D1.a0 += A.a0.y; D1.a1 += A.a1.y; D1.a2 += A.a2.y;
 }
 
-__global__ void __launch_bounds__(NT) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
+__global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             const float4* __restrict__ pos, const float4* __restrict__ alp,
@@ -140,7 +165,8 @@ __global__ void __launch_bounds__(NT) k_p2p(const int* __restrict__ leaf_ids, co
   for (int t0 = 0; t0 < tcnt; t0 += TP) {
     const int i0 = t0 + lane, i1 = t0 + lane + NT;
     const bool v0 = i0 < tcnt, v1 = i1 < tcnt;
-    float x00 = 0.f, x01 = 0.f, x02 = 0.f, x10 = 0.f, x11 = 0.f, x12 = 0.f;
+    // absent targets sit far away so they never trigger the close-pair branch
+    float x00 = 1e4f, x01 = 1e4f, x02 = 1e4f, x10 = 1e4f, x11 = 1e4f, x12 = 1e4f;
     float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
     if (v0) {
       const float4 p = pos[tb + i0];
@@ -189,26 +215,18 @@ __global__ void __launch_bounds__(NT) k_p2p(const int* __restrict__ leaf_ids, co
         const int nj = min(TP, scnt - s0);
         // every pair of this tile has rho >= 4.5 => exact singular branch
         const bool far = dmin2 >= 40.5f * smax * smax;
-        Acc A0, A1;
-        zero(A0);
-        zero(A1);
+        Acc2 A;
+        zero(A);
+        const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
+        const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
         if (far) {
 #pragma unroll 4
-          for (int jj = 0; jj < nj; ++jj) {
-            const float4 q = sx[jj], a = sa[jj];
-            pair<false>(A0, x00, x01, x02, a0.x, a0.y, a0.z, q, a);
-            pair<false>(A1, x10, x11, x12, a1.x, a1.y, a1.z, q, a);
-          }
+          for (int jj = 0; jj < nj; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
         } else {
 #pragma unroll 2
-          for (int jj = 0; jj < nj; ++jj) {
-            const float4 q = sx[jj], a = sa[jj];
-            pair<true>(A0, x00, x01, x02, a0.x, a0.y, a0.z, q, a);
-            pair<true>(A1, x10, x11, x12, a1.x, a1.y, a1.z, q, a);
-          }
+          for (int jj = 0; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
         }
-        flush(D0, A0);
-        flush(D1, A1);
+        flush(D0, D1, A);
       }
     }
     // s += (sum_j f alpha_j) x alpha_i
