@@ -297,14 +297,26 @@ def main():
 
     if rank == 0:
         traffic, prof = load_profile_traffic()
-        achieved = FLOPS_PER_PAIR * pairs / (phase["ms_p2p"] * 1e-3) / 1e12
+        from tools.sass_flops import p2p_flops_per_pair
+        fpp = p2p_flops_per_pair(P.fmm.LIB_PATH)
+        near = statistics.mean(st["p2p_near_pairs"] for st in stats)
+        hw_flops = near * fpp.get("near", 0.0) + (pairs - near) * fpp.get("far", 0.0)
+        t_p2p = phase["ms_p2p"] * 1e-3
+        achieved = hw_flops / t_p2p / 1e12
         roof = {"kernel": "k_p2p (near field, a12)", "bound": "alu", "achieved": achieved,
                 "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
                 "traffic": traffic,
-                "note": "achieved = 174 model flop/pair (Table 1) x pairs / mean P2P launch time (CUDA events on the "
-                        "launch stream); peak = 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"}
+                "per_launch": {"ms": phase["ms_p2p"], "pairs": pairs, "near_pairs": int(near),
+                               "hw_flops_per_pair": fpp, "hw_flops": hw_flops},
+                "model": {"flops_per_pair": FLOPS_PER_PAIR,
+                          "achieved_tflops": FLOPS_PER_PAIR * pairs / t_p2p / 1e12,
+                          "note": "paper-style Table 1 count (sqrt/rsqrt/exp/div = 1 flop); not a hardware rate"},
+                "note": "achieved = FP32 FADD/FMUL (1) + FFMA (2) per pair counted from the kernel's SASS "
+                        "(tools/sass_flops.py; packed FP32x2 ops count per lane) x pairs on each tile kind / "
+                        "mean P2P launch time (CUDA events on the launch stream); peak = 148 SM x 128 FP32 lanes "
+                        "x 2 x 1.965 GHz (derived, DESIGN.md; FFMA/FFMA2 probe measured 72.4/73.9 TFLOP/s)"}
         if prof:
-            roof["hw"] = {k: prof[k] for k in prof if k != "dram_bytes_per_launch"}
+            roof["profile"] = {k: prof[k] for k in prof if k != "dram_bytes_per_launch"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:

@@ -87,6 +87,8 @@ typedef struct {
   double   model_flops;          /* 174 * p2p_pairs (Table 1)               */
   int64_t  launches;             /* this library's kernel launches since set_particles */
   int64_t  cub_calls;            /* CUB device-wide calls (radix sort, scan) since then */
+  int64_t  p2p_near_pairs;       /* pairs of P2P tiles evaluated with the cutoff g (the
+                                    rest took the exact singular branch, rho >= 4.5)   */
   double   ms_keys, ms_sort, ms_tree;                  /* set_particles: a1-a4         */
   double   ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_downward, ms_finalize;
   double   ms_set_total, ms_eval_total;

@@ -120,7 +120,10 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
   if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaEventRecord(c.ev[PH_FIN], st));
+  unsigned long long nnear = 0;
+  if (c.nleaves > 0) FMM_CUDA(cudaMemcpyAsync(&nnear, c.dnear.p, sizeof(nnear), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
+  c.p2p_near_pairs = (int64_t)nnear;
   c.evaluated = true;
   fmm_stats& S = c.stats;
   S.ms_upward = ms_between(c.ev[PH_EVAL0], c.ev[PH_UP]);
@@ -263,6 +266,7 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->far_m2l = c.far_m2l;
   s->model_flops = 174.0 * (double)c.p2p_pairs;
   s->launches = c.launches;
+  s->p2p_near_pairs = c.p2p_near_pairs;
   s->cub_calls = c.cub_calls;
   return FMM_OK;
 }

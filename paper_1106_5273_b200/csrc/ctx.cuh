@@ -51,7 +51,8 @@ struct Ctx {
   DBuf<int> cnt_m2l, cnt_p2p, cnt_push, off_m2l, off_p2p, off_push;
   int64_t np2p = 0, nm2l = 0, p2p_pairs = 0;
   DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;
-  DBuf<unsigned long long> dcount;
+  DBuf<unsigned long long> dcount, dnear;
+  int64_t p2p_near_pairs = 0;                // pairs of the last P2P on regularised tiles
 
   // ---- expansions and results ----
   DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)

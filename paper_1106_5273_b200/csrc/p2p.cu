@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             const float4* __restrict__ pos, const float4* __restrict__ alp,
-                                            float* __restrict__ un, float* __restrict__ sn) {
+                                            float* __restrict__ un, float* __restrict__ sn,
+                                            unsigned long long* __restrict__ near_pairs) {
   __shared__ float4 sx[TP];   // (x', y', z', -1/(2 sigma^2))
   __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
   const float k4 = (float)(1.0 / (4.0 * kPi));
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
   const double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s,
                cz = lo2 + (c.qz[leaf] + 0.5) * s;
   const int eb = seg_b[leaf], ee = seg_e[leaf];
+  unsigned long long nnear = 0;                   // pairs evaluated with the regularised kernel
   for (int t0 = 0; t0 < tcnt; t0 += TP) {
     const int i0 = t0 + lane, i1 = t0 + lane + NT;
     const bool v0 = i0 < tcnt, v1 = i1 < tcnt;
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
         const int nj = min(TP, scnt - s0);
         // every pair of this tile has rho >= 4.5 => exact singular branch
         const bool far = dmin2 >= 40.5f * smax * smax;
+        if (!far) nnear += (unsigned long long)nj * (unsigned long long)min(TP, tcnt - t0);
         Acc2 A;
         zero(A);
         const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
       sn[o + 2] = (float)(D1.s2 + (D1.a0 * a1.y - D1.a1 * a1.x));
     }
   }
+  if (lane == 0 && nnear) atomicAdd(near_pairs, nnear);
 }
 
 __global__ void k_eval_cutoff(const float* __restrict__ rho, int64_t n, float* __restrict__ g) {
@@ -259,9 +263,11 @@ __global__ void k_eval_cutoff(const float* __restrict__ rho, int64_t n, float* _
 
 void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   if (c.nleaves == 0) return;
+  c.dnear.reserve(1);
+  FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
-             c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near);
+             c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near, c.dnear.p);
 }
 
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {

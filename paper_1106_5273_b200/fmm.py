@@ -32,7 +32,7 @@ class fmm_stats(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("n", C.c_int64), ("ncells", C.c_int64), ("nleaves", C.c_int64),
                 ("nlevels", C.c_int64), ("p2p_list", C.c_int64), ("m2l_list", C.c_int64),
                 ("p2p_pairs", C.c_int64), ("far_m2l", C.c_int64), ("model_flops", C.c_double),
-                ("launches", C.c_int64), ("cub_calls", C.c_int64),
+                ("launches", C.c_int64), ("cub_calls", C.c_int64), ("p2p_near_pairs", C.c_int64),
                 ("ms_keys", C.c_double), ("ms_sort", C.c_double), ("ms_tree", C.c_double),
                 ("ms_upward", C.c_double), ("ms_traverse", C.c_double), ("ms_m2l", C.c_double),
                 ("ms_p2p", C.c_double), ("ms_downward", C.c_double), ("ms_finalize", C.c_double),
