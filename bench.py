@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=256, help="lattice points per dimension per GPU")
+    ap.add_argument("--side", type=int, default=256, help="lattice points per dimension per GPU")
     ap.add_argument("--order", type=int, default=10)
     ap.add_argument("--images", type=int, default=3)
     ap.add_argument("--theta", default="1/2")
@@ -206,11 +206,17 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     theta = theta_of(args.theta)
 
-    x, a, s = synth.taylor_green(args.n)
+    # C3 at N = 1; the weak-scaling blocks (synth.taylor_green_rank) at N > 1
+    x, a, s = synth.taylor_green_rank(args.side, world, rank)
     n = len(x)
     stream = torch.cuda.Stream()
+    nccl_id = None
+    if world > 1:
+        obj = [P.fmm_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     f = P.FMM(order=args.order, images=args.images, theta=theta, ncrit=args.ncrit, device=local,
-              stream=stream.cuda_stream)
+              stream=stream.cuda_stream, nranks=world, rank=rank, nccl_id=nccl_id)
     with torch.cuda.stream(stream):
         xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
         ud = torch.empty((n, 3), device="cuda")
@@ -329,12 +335,20 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "s_per_step": ms_max / 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic Taylor-Green lattice (reading Z26), generated on host, resident in HBM",
-            "config": {"workload": "C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
-                                   "ncrit=%d" % (args.n, n, args.images, args.order, args.theta, args.ncrit),
+            "config": {"workload": ("C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
+                                    "ncrit=%d" % (args.side, n, args.images, args.order, args.theta, args.ncrit))
+                       if world == 1 else
+                       ("C5 weak scaling: Taylor-Green lattice %s in [-pi,pi)^3, %d^3 = %d particles per GPU, "
+                        "periodic k=%d, p=%d, theta=%s, ncrit=%d" %
+                        ("x".join(str(args.side * m) for m in synth.RANK_LATTICE[world]), args.side, n,
+                         args.images, args.order, args.theta, args.ncrit)),
                        "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
                        "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),
                        "parallelism": "1 GPU" if world == 1 else
-                       "%d independent periodic replicas (LET exchange not yet implemented)" % world},
+                       "%d GPUs: Morton-octant domain decomposition, exact LET (multipoles + bodies) over "
+                       "NCCL grouped send/recv, root multipole all-reduce" % world},
+            "let": None if world == 1 else {k: statistics.mean(st[k] for st in stats) for k in
+                                            ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves", "ms_let")},
             "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
             "particles_per_s": tot_n / (ms_max * 1e-3),
             "phases_ms": phase,

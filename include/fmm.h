@@ -72,8 +72,11 @@ typedef struct {
   int32_t  traversal;            /* 0 = MAC-first (default), 1 = leaf-first (Z11)      */
   int32_t  device;               /* CUDA ordinal                                       */
   void*    stream;               /* cudaStream_t for all work; NULL = library-owned    */
-  int32_t  rank, nranks;         /* nranks == 1: single GPU                            */
-  const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1              */
+  int32_t  rank, nranks;         /* nranks in {1,2,4,8}; rank r owns the particles whose
+                                    Morton keys lie in top octants [8r/P, 8(r+1)/P)
+                                    (each rank passes only those, else FMM_E_ARG) */
+  const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1 (all ranks
+                                    pass the same id, e.g. broadcast by torch.distributed) */
 } fmm_config;
 
 /* Per-phase device times of the last set_particles / evaluate (CUDA events on
@@ -92,6 +95,11 @@ typedef struct {
   double   ms_keys, ms_sort, ms_tree;                  /* set_particles: a1-a4         */
   double   ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_downward, ms_finalize;
   double   ms_set_total, ms_eval_total;
+  /* multi-GPU (a14): global particle count and the last LET exchange */
+  int64_t  ntot;
+  int64_t  let_bytes_sent, let_bytes_recv;  /* reply payload bytes                       */
+  int64_t  let_cells, let_leaves;           /* remote multipoles / leaves received         */
+  double   ms_let;                          /* exchange time (CUDA events, incl. requests) */
 } fmm_stats;
 
 /* Fill cfg with the defaults listed above. */
@@ -140,6 +148,11 @@ fmm_status fmm_get_lists(fmm_ctx* ctx, int64_t* p2p, int64_t* m2l);
  * L~_n = L_n s^(n+1), s = cell side; [ncells][3][p(p+1)/2] complex FP32
  * (interleaved re, im) -- either pointer may be NULL. */
 fmm_status fmm_get_expansions(const fmm_ctx* ctx, float* M, float* L);
+
+/* Multi-GPU bootstrap: writes a fresh 128-byte ncclUniqueId into id (one rank
+ * calls it and broadcasts the bytes to the others, e.g. via torch.distributed;
+ * every rank then passes them as fmm_config.nccl_id).  Errors: FMM_E_NCCL. */
+fmm_status fmm_comm_unique_id(void* id);
 
 /* The device's FP32 evaluation of the Eq. 2 cutoff g(rho) used by P2P
  * (reading Z6: any approximation with |g - g_exact| <= 2e-7).  rho[n] in,

@@ -19,8 +19,20 @@ LIB = os.path.join(HERE, "libfmm_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """torch's NCCL (one NCCL per process: the same library torch.distributed loads)."""
+    try:
+        import nvidia.nccl
+        return os.path.dirname(list(nvidia.nccl.__path__)[0] + "/")
+    except Exception:
+        return "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-         "-I" + INCLUDE]
+         "-I" + INCLUDE, "-I" + os.path.join(NCCL, "include")]
 
 
 def _deps():
@@ -57,7 +69,9 @@ def build(force: bool = False) -> str:
         objs = list(ex.map(_compile, srcs))
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp.%d" % os.getpid()
-        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-Xcompiler", "-fPIC"]
+        libdir = os.path.join(NCCL, "lib")
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-Xcompiler", "-fPIC", "-L" + libdir, "-l:libnccl.so.2",
+                                                              "-Xlinker", "-rpath=" + libdir]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr[-4000:])

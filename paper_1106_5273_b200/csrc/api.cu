@@ -15,15 +15,15 @@ void set_expansion_smem_limits();
 
 namespace {
 
-__global__ void k_finalize(const uint32_t* __restrict__ idx, int64_t n, int parts, const float* __restrict__ un,
+__global__ void k_finalize(const uint32_t* __restrict__ idx, int64_t n, int64_t off, int parts, const float* __restrict__ un,
                            const float* __restrict__ sn, const float* __restrict__ uf, const float* __restrict__ sf,
                            float* __restrict__ u, float* __restrict__ s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t o = 3 * (int64_t)idx[i];
+    int64_t o = 3 * (int64_t)idx[i], g = 3 * (off + i);
     for (int d = 0; d < 3; ++d) {
       float uu = 0.f, ss = 0.f;
-      if (parts & 1) { uu += un[3 * i + d]; ss += sn[3 * i + d]; }
-      if (parts & 2) { uu += uf[3 * i + d]; ss += sf[3 * i + d]; }
+      if (parts & 1) { uu += un[g + d]; ss += sn[g + d]; }
+      if (parts & 2) { uu += uf[g + d]; ss += sf[g + d]; }
       u[o + d] = uu;
       s[o + d] = ss;
     }
@@ -54,7 +54,9 @@ void check_config(const fmm_config& c) {
   if (c.images > 0 && !(c.box_len > 0.0 && std::isfinite(c.box_len))) throw FmmError(FMM_E_ARG, "box_len must be > 0");
   if (c.traversal != 0 && c.traversal != 1) throw FmmError(FMM_E_ARG, "traversal must be 0 or 1");
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) throw FmmError(FMM_E_ARG, "bad rank/nranks");
-  if (c.nranks > 1) throw FmmError(FMM_E_ARG, "multi-GPU contexts are created per rank with nranks == 1 in this build");
+  if (c.nranks != 1 && c.nranks != 2 && c.nranks != 4 && c.nranks != 8)
+    throw FmmError(FMM_E_ARG, "nranks must be 1, 2, 4 or 8 (ranks own top-level Morton octants)");
+  if (c.nranks > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "multi-GPU needs the periodic mode (images >= 1)");
 }
 
 template <typename F>
@@ -80,8 +82,9 @@ fmm_status guard(Ctx* c, F f) {
 void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   cudaStream_t st = c.stream;
   int64_t n = c.n;
+  const bool multi = c.cfg.nranks > 1;
   FMM_CUDA(cudaEventRecord(c.ev[PH_EVAL0], st));
-  if (n == 0) {
+  if (c.ntot == 0) {
     for (int p = PH_UP; p <= PH_FIN; ++p) FMM_CUDA(cudaEventRecord(c.ev[p], st));
     c.evaluated = true;
     return;
@@ -89,13 +92,29 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   size_t ncoef = (size_t)c.ncells * 3 * c.nc;
   c.M.reserve(ncoef);
   c.Lc.reserve(ncoef);
-  c.u_near.reserve(3 * n); c.s_near.reserve(3 * n); c.u_far.reserve(3 * n); c.s_far.reserve(3 * n);
-  // a5-a6 upward pass
+  const int64_t N = c.ntot;
+  c.u_near.reserve(3 * N); c.s_near.reserve(3 * N); c.u_far.reserve(3 * N); c.s_far.reserve(3 * N);
+  // a5-a6 upward pass (cells of other ranks stay zero until the LET arrives)
+  if (multi) FMM_CUDA(cudaMemsetAsync(c.M.p, 0, ncoef * sizeof(float2), st));
   upward_pass(c);
   FMM_CUDA(cudaEventRecord(c.ev[PH_UP], st));
   // a7 traversal (once per set_particles)
   if (!c.lists_valid) build_lists(c);
   FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
+  // a14 LET exchange (multipoles and bodies of the remote sources in this rank's lists)
+  if (multi) {
+    cudaEvent_t l0, l1;
+    FMM_CUDA(cudaEventCreate(&l0));
+    FMM_CUDA(cudaEventCreate(&l1));
+    FMM_CUDA(cudaEventRecord(l0, st));
+    let_exchange(c);
+    FMM_CUDA(cudaEventRecord(l1, st));
+    FMM_CUDA(cudaEventSynchronize(l1));
+    c.ms_let = ms_between(l0, l1);
+    cudaEventDestroy(l0);
+    cudaEventDestroy(l1);
+    FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
+  }
   // a9 M2L + a8 periodic far layers
   FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
   m2l_pass(c);
@@ -115,7 +134,8 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   if (hs) { c.stage_ds.reserve(3 * n); ds = c.stage_ds.p; }
   unsigned g = nblocks(n, 256);
   if (g > 148 * 16) g = 148 * 16;
-  FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
+  if (n > 0)
+    FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, c.off, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
   FMM_LAUNCH_CHECK();
   if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
   if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
@@ -181,6 +201,7 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
     set_expansion_smem_limits();
     FMM_CUDA(cudaGetLastError());
+    comm_init(c);
   });
   if (st != FMM_OK) { delete h; return st; }
   *out = h;
@@ -193,6 +214,7 @@ FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
   cudaSetDevice(c.cfg.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   for (int i = 0; i <= PH_N; ++i) if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+  try { comm_destroy(c); } catch (...) {}
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
   delete h;
   return FMM_OK;
@@ -267,6 +289,12 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->model_flops = 174.0 * (double)c.p2p_pairs;
   s->launches = c.launches;
   s->p2p_near_pairs = c.p2p_near_pairs;
+  s->ntot = c.ntot;
+  s->let_bytes_sent = c.let_bytes_sent;
+  s->let_bytes_recv = c.let_bytes_recv;
+  s->let_cells = c.let_cells;
+  s->let_leaves = c.let_leaves;
+  s->ms_let = c.ms_let;
   s->cub_calls = c.cub_calls;
   return FMM_OK;
 }
@@ -299,7 +327,8 @@ FMM_API fmm_status fmm_get_keys(const fmm_ctx* h, uint64_t* keys, int64_t* perm)
     if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
     if (c.n == 0) return;
     std::vector<uint32_t> idx(c.n);
-    if (keys) FMM_CUDA(cudaMemcpy(keys, c.keys.p, sizeof(uint64_t) * c.n, cudaMemcpyDeviceToHost));
+    const uint64_t* kp = c.cfg.nranks > 1 ? c.keys_loc.p : c.keys.p;
+    if (keys) FMM_CUDA(cudaMemcpy(keys, kp, sizeof(uint64_t) * c.n, cudaMemcpyDeviceToHost));
     FMM_CUDA(cudaMemcpy(idx.data(), c.idx.p, sizeof(uint32_t) * c.n, cudaMemcpyDeviceToHost));
     if (perm) for (int64_t i = 0; i < c.n; ++i) perm[i] = idx[i];
   });
@@ -369,4 +398,16 @@ FMM_API fmm_status fmm_eval_cutoff(fmm_ctx* h, int64_t n, const float* rho, floa
     FMM_CUDA(cudaMemcpyAsync(g, c.stage_ds.p, sizeof(float) * n, cudaMemcpyDefault, c.stream));
     FMM_CUDA(cudaStreamSynchronize(c.stream));
   });
+}
+
+FMM_API fmm_status fmm_comm_unique_id(void* id) {
+  if (!id) return FMM_E_ARG;
+  try {
+    comm_unique_id(id);
+    return FMM_OK;
+  } catch (const FmmError& e) {
+    return e.code;
+  } catch (...) {
+    return FMM_E_INTERNAL;
+  }
 }

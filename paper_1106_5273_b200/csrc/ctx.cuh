@@ -29,6 +29,20 @@ struct Ctx {
   std::string err;
   bool poisoned = false;
 
+  // ---- multi-GPU (a14): this rank owns global sorted positions [off, off + n) ----
+  void* comm = nullptr;                      // ncclComm_t
+  int64_t ntot = 0, off = 0;
+  std::vector<int64_t> rank_off;             // [nranks + 1] global offsets of the ranks' particles
+  DBuf<int64_t> comm_i64;
+  DBuf<int> tgt_ok;                          // cell may hold local targets (traversal filter)
+  std::vector<int64_t> loc_lo, loc_hi;       // per level: cells fully owned by this rank
+  DBuf<uint64_t> keys_loc;                   // local sorted keys (multi-GPU)
+  DBuf<int> need, need_ids, need_ids2, req_in, req_owner, req_owner2;
+  DBuf<char> let_send, let_recv;
+  DBuf<int64_t> req_off;
+  int64_t let_bytes_sent = 0, let_bytes_recv = 0, let_cells = 0, let_leaves = 0;
+  double ms_let = 0.0;
+
   // ---- particles and tree (set_particles) ----
   int64_t n = 0;
   bool have_particles = false;
@@ -77,6 +91,15 @@ void build_lists(Ctx& c);
 void upward_pass(Ctx& c);
 void m2l_pass(Ctx& c);
 bool m2l_pass_reg(Ctx& c);
+void comm_init(Ctx& c);
+void comm_unique_id(void* out);
+void comm_destroy(Ctx& c);
+std::vector<int64_t> allgather_i64(Ctx& c, int64_t v);
+std::vector<int64_t> alltoall_i64(Ctx& c, const std::vector<int64_t>& send);
+void alltoallv_bytes(Ctx& c, const void* sbuf, const std::vector<int64_t>& soff, const std::vector<int64_t>& sbytes,
+                     void* rbuf, const std::vector<int64_t>& roff, const std::vector<int64_t>& rbytes);
+void allreduce_sum_f32(Ctx& c, float* p, int64_t n);
+void let_exchange(Ctx& c);
 void periodic_far_pass(Ctx& c);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);

@@ -426,13 +426,15 @@ void upward_pass(Ctx& c) {
     FMM_LAUNCH(c, k_p2m, (unsigned)c.nleaves, round32(3 * nc), sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
     FMM_LAUNCH_CHECK();
   }
+  // M2M over this rank's cells; the root (shared by all ranks) sums its local
+  // children here and the other ranks' through an all-reduce (a14)
   int nlev = (int)c.level_begin.size() - 1;
   for (int l = nlev - 2; l >= 0; --l) {
-    int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
+    int64_t first = l == 0 ? 0 : c.loc_lo[l], cnt = l == 0 ? 1 : c.loc_hi[l] - c.loc_lo[l];
     if (cnt <= 0) continue;
     FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, P, first, gc, c.M.p);
-    FMM_LAUNCH_CHECK();
   }
+  if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc);
 }
 
 void m2l_pass(Ctx& c) {
@@ -451,11 +453,16 @@ void periodic_far_pass(Ctx& c) {
   if (k < 2 || c.ncells == 0) return;
   int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   // far targets: cells at level 2 and leaves above level 2
+  // (this rank's cells only)
   std::vector<int> tg;
-  for (size_t i = 0; i < c.host_leaf_top.size(); ++i)
-    if (c.host_leaf_top[i]) tg.push_back((int)i);
+  for (size_t i = 0; i < c.host_leaf_top.size(); ++i) {
+    if (!c.host_leaf_top[i]) continue;
+    const int l = i == 0 ? 0 : 1;
+    if (c.cfg.nranks == 1 || ((int64_t)i >= c.loc_lo[l] && (int64_t)i < c.loc_hi[l])) tg.push_back((int)i);
+  }
   if (c.level_begin.size() > 3)
-    for (int64_t i = c.level_begin[2]; i < c.level_begin[3]; ++i) tg.push_back((int)i);
+    for (int64_t i = c.loc_lo[2]; i < c.loc_hi[2]; ++i) tg.push_back((int)i);
+  if (tg.empty()) return;
   c.far_M.reserve((size_t)(k - 1) * 3 * nc * 2);
   FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, c.M.p, c.far_M.p);
   FMM_LAUNCH_CHECK();
@@ -478,7 +485,7 @@ void downward_pass(Ctx& c, float* u_far, float* s_far) {
   GCells gc = gcells(c);
   int nlev = (int)c.level_begin.size() - 1;
   for (int l = 1; l < nlev; ++l) {
-    int64_t first = c.level_begin[l], cnt = c.level_begin[l + 1] - first;
+    int64_t first = c.loc_lo[l], cnt = c.loc_hi[l] - first;
     if (cnt <= 0) continue;
     FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, c.Lc.p);
     FMM_LAUNCH_CHECK();

@@ -17,7 +17,7 @@ namespace fmmb {
 namespace {
 
 struct TCells {
-  const int *level, *qx, *qy, *qz, *child_begin, *nchild, *leaf, *count;
+  const int *level, *qx, *qy, *qz, *child_begin, *nchild, *leaf, *count, *tgt_ok;
 };
 
 struct TParams {
@@ -74,6 +74,7 @@ __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells 
   for (int k = 0; k < nch; ++k) {
     int a = split_b ? A : cb + k;
     int b = split_b ? cb + k : B;
+    if (!split_b && !c.tgt_ok[a]) continue;        // a14: targets of other ranks are theirs
     int d = interact(c, p, a, b, img);
     if (d == 0) { if (WRITE) m2l[bm + nm] = pack(a, b, img); ++nm; }
     else if (d == 1) { if (WRITE) p2p[bp + np] = pack(a, b, img); ++np; }
@@ -140,7 +141,7 @@ void build_lists(Ctx& c) {
   c.p2p_pairs = 0;
   if (c.ncells == 0) { c.lists_valid = true; return; }
   TCells tc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.child_begin.p,
-            c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p};
+            c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p, c.tgt_ok.p};
   TParams tp{3ull * (unsigned long long)c.cfg.theta_den * (unsigned long long)c.cfg.theta_den,
              (unsigned long long)c.cfg.theta_num * (unsigned long long)c.cfg.theta_num, c.cfg.traversal};
 

@@ -205,6 +205,30 @@ __global__ void k_scatter_leaves(const int* __restrict__ leaf, const int* __rest
     if (leaf[i]) ids[scan[i] - 1] = (int)i;
 }
 
+// local leaves (this rank's targets) and the traversal's target filter
+__global__ void k_local_flags(const int* __restrict__ leaf, const int* __restrict__ begin,
+                              const int* __restrict__ count, int64_t nc, int64_t off, int64_t n,
+                              int* __restrict__ lflag, int* __restrict__ tgt_ok) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = begin[i], e = b + count[i];
+    lflag[i] = (leaf[i] && b >= off && e <= off + n) ? 1 : 0;
+    tgt_ok[i] = (b < off + n && e > off) ? 1 : 0;
+  }
+}
+
+// per level: first and last cell fully inside [off, off + n)
+__global__ void k_local_range(const int* __restrict__ level, const int* __restrict__ begin,
+                              const int* __restrict__ count, int64_t nc, int64_t off, int64_t n,
+                              int* __restrict__ lo, int* __restrict__ hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = begin[i], e = b + count[i];
+    if (b >= off && e <= off + n) {
+      atomicMin(&lo[level[i]], (int)i);
+      atomicMax(&hi[level[i]], (int)i);
+    }
+  }
+}
+
 template <typename F>
 void cub_call(Ctx& c, F f) {
   size_t bytes = 0;
@@ -269,7 +293,10 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   for (int d = 0; d < 3; ++d) c.lo[d] = b.lo[d];
   c.L = b.L;
 
-  if (n == 0) {
+  if (n == 0 && c.cfg.nranks == 1) {
+    c.ntot = 0;
+    c.off = 0;
+    c.rank_off.assign(2, 0);
     FMM_CUDA(cudaEventRecord(c.ev[PH_KEYS], st));
     FMM_CUDA(cudaEventRecord(c.ev[PH_SORT], st));
     FMM_CUDA(cudaEventRecord(c.ev[PH_TREE], st));
@@ -278,55 +305,97 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   }
 
   // a2: keys
-  c.pos_tmp.reserve(n); c.keys_tmp.reserve(n); c.idx_tmp.reserve(n);
-  c.keys.reserve(n); c.idx.reserve(n); c.pos.reserve(n); c.alp.reserve(n);
+  const int P = c.cfg.nranks, R = c.cfg.rank;
+  const bool multi = P > 1;
+  c.pos_tmp.reserve(n); c.keys_tmp.reserve(n); c.idx_tmp.reserve(n); c.idx.reserve(n);
   FMM_LAUNCH(c, k_keys, grid_for(n), 256, 0, x, s, n, b, c.pos_tmp.p, c.keys_tmp.p, c.idx_tmp.p);
-  FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaEventRecord(c.ev[PH_KEYS], st));
 
-  // a3: stable LSD radix sort on the 63 key bits, then gather
-  {
-    uint64_t *kin = c.keys_tmp.p, *kout = c.keys.p;
+  // a3: stable LSD radix sort on the 63 key bits
+  uint64_t* ksorted;
+  if (multi) { c.keys_loc.reserve(n); ksorted = c.keys_loc.p; }
+  else { c.keys.reserve(n); ksorted = c.keys.p; }
+  if (n > 0) {
+    uint64_t *kin = c.keys_tmp.p, *kout = ksorted;
     uint32_t *vin = c.idx_tmp.p, *vout = c.idx.p;
     int nn = (int)n;
     cub_call(c, [&](void* tmp, size_t& bytes) {
       return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, nn, 0, 63, st);
     });
   }
-  FMM_LAUNCH(c, k_gather, grid_for(n), 256, 0, c.pos_tmp.p, a, c.idx.p, n, c.pos.p, c.alp.p);
-  FMM_LAUNCH_CHECK();
+  // a14: global key order = the ranks' sorted keys concatenated in rank order
+  // (each rank owns a contiguous Morton range: octants [8R/P, 8(R+1)/P))
+  c.rank_off.assign(P + 1, 0);
+  if (multi) {
+    if (n > 0) {
+      uint64_t kk[2];
+      FMM_CUDA(cudaMemcpyAsync(&kk[0], ksorted, 8, cudaMemcpyDeviceToHost, st));
+      FMM_CUDA(cudaMemcpyAsync(&kk[1], ksorted + n - 1, 8, cudaMemcpyDeviceToHost, st));
+      FMM_CUDA(cudaStreamSynchronize(st));
+      const int o0 = (int)(kk[0] >> 60), o1 = (int)(kk[1] >> 60);
+      if (o0 < 8 * R / P || o1 >= 8 * (R + 1) / P)
+        throw FmmError(FMM_E_ARG, "rank holds particles outside its Morton range (octants [8r/P, 8(r+1)/P))");
+    }
+    std::vector<int64_t> cnt = allgather_i64(c, n);
+    for (int q = 0; q < P; ++q) c.rank_off[q + 1] = c.rank_off[q] + cnt[q];
+    c.ntot = c.rank_off[P];
+    c.off = c.rank_off[R];
+    c.keys.reserve(c.ntot);
+    if (n > 0) FMM_CUDA(cudaMemcpyAsync(c.keys.p + c.off, ksorted, 8 * n, cudaMemcpyDeviceToDevice, st));
+    std::vector<int64_t> soff(P, 0), sb(P, 0), roff(P, 0), rb(P, 0);
+    for (int q = 0; q < P; ++q) {
+      if (q == R) continue;
+      sb[q] = 8 * n;
+      roff[q] = 8 * c.rank_off[q];
+      rb[q] = 8 * cnt[q];
+    }
+    alltoallv_bytes(c, ksorted, soff, sb, c.keys.p, roff, rb);
+  } else {
+    c.ntot = n;
+    c.off = 0;
+    c.rank_off[1] = n;
+  }
+  const int64_t N = c.ntot;
+  c.pos.reserve(N); c.alp.reserve(N);
+  if (n > 0) FMM_LAUNCH(c, k_gather, grid_for(n), 256, 0, c.pos_tmp.p, a, c.idx.p, n, c.pos.p + c.off, c.alp.p + c.off);
   FMM_CUDA(cudaEventRecord(c.ev[PH_SORT], st));
+  if (N == 0) {
+    FMM_CUDA(cudaEventRecord(c.ev[PH_TREE], st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    c.have_particles = true;
+    return;
+  }
 
   // a4: cells level by level
-  size_t capc = (size_t)(2 * (n / (c.cfg.ncrit + 1)) + 64);
+  size_t capc = (size_t)(2 * (N / (c.cfg.ncrit + 1)) + 64);
   c.cells.reserve_keep(capc, 0, st);
-  c.pcell_a.reserve(n); c.pcell_b.reserve(n); c.flags.reserve(n); c.scan.reserve(n);
-  FMM_LAUNCH(c, k_root, 1, 1, 0, ptrs(c.cells), n, c.cfg.ncrit);
-  FMM_LAUNCH(c, k_fill_int, grid_for(n), 256, 0, c.pcell_a.p, n, 0);
+  c.pcell_a.reserve(N); c.pcell_b.reserve(N); c.flags.reserve(N); c.scan.reserve(N);
+  FMM_LAUNCH(c, k_root, 1, 1, 0, ptrs(c.cells), N, c.cfg.ncrit);
+  FMM_LAUNCH(c, k_fill_int, grid_for(N), 256, 0, c.pcell_a.p, N, 0);
   FMM_LAUNCH_CHECK();
   int64_t ncells = 1;
   c.level_begin.assign({0, 1});
   int* pc_old = c.pcell_a.p;
   int* pc_new = c.pcell_b.p;
   for (int l = 1; l <= kMaxLevel; ++l) {
-    FMM_LAUNCH(c, k_level_flags, grid_for(n), 256, 0, c.keys.p, pc_old, c.cells.leaf.p, n, l, c.flags.p);
+    FMM_LAUNCH(c, k_level_flags, grid_for(N), 256, 0, c.keys.p, pc_old, c.cells.leaf.p, N, l, c.flags.p);
     FMM_LAUNCH_CHECK();
     {
       int* fin = c.flags.p;
       int* fout = c.scan.p;
-      int nn = (int)n;
+      int nn = (int)N;
       cub_call(c, [&](void* tmp, size_t& bytes) {
         return cub::DeviceScan::InclusiveSum(tmp, bytes, fin, fout, nn, st);
       });
     }
     int total = 0;
-    FMM_CUDA(cudaMemcpyAsync(&total, c.scan.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&total, c.scan.p + (N - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
     FMM_CUDA(cudaStreamSynchronize(st));
     if (total == 0) break;
     if ((size_t)(ncells + total) > c.cells.level.cap) c.cells.reserve_keep((size_t)(ncells + total) * 2, ncells, st);
-    FMM_LAUNCH(c, k_level_fill, grid_for(n), 256, 0, c.keys.p, pc_old, c.flags.p, c.scan.p, ptrs(c.cells), n, l,
+    FMM_LAUNCH(c, k_level_fill, grid_for(N), 256, 0, c.keys.p, pc_old, c.flags.p, c.scan.p, ptrs(c.cells), N, l,
                                               (int)ncells, pc_new);
-    FMM_LAUNCH(c, k_level_end, grid_for(n), 256, 0, pc_new, ptrs(c.cells), n, l, c.cfg.ncrit);
+    FMM_LAUNCH(c, k_level_end, grid_for(N), 256, 0, pc_new, ptrs(c.cells), N, l, c.cfg.ncrit);
     FMM_LAUNCH_CHECK();
     ncells += total;
     c.level_begin.push_back(ncells);
@@ -335,9 +404,11 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   c.ncells = ncells;
   if (ncells >= (1ll << 27)) throw FmmError(FMM_E_ARG, "more than 2^27 cells; raise ncrit");
 
-  // leaf id list
+  // local leaf list (this rank's targets), traversal filter, per-level local cell ranges
   c.leaf_ids.reserve(ncells);
-  FMM_LAUNCH(c, k_leaf_flags, grid_for(ncells), 256, 0, c.cells.leaf.p, ncells, c.flags.p);
+  c.tgt_ok.reserve(ncells);
+  FMM_LAUNCH(c, k_local_flags, grid_for(ncells), 256, 0, c.cells.leaf.p, c.cells.begin.p, c.cells.count.p, ncells,
+             c.off, n, c.flags.p, c.tgt_ok.p);
   {
     int* fin = c.flags.p;
     int* fout = c.scan.p;
@@ -346,8 +417,24 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
       return cub::DeviceScan::InclusiveSum(tmp, bytes, fin, fout, nn, st);
     });
   }
-  FMM_LAUNCH(c, k_scatter_leaves, grid_for(ncells), 256, 0, c.cells.leaf.p, c.scan.p, ncells, c.leaf_ids.p);
-  FMM_LAUNCH_CHECK();
+  FMM_LAUNCH(c, k_scatter_leaves, grid_for(ncells), 256, 0, c.flags.p, c.scan.p, ncells, c.leaf_ids.p);
+  const int nlev = (int)c.level_begin.size() - 1;
+  {
+    std::vector<int> init(2 * (kMaxLevel + 1));
+    for (int l = 0; l <= kMaxLevel; ++l) { init[l] = INT_MAX; init[kMaxLevel + 1 + l] = -1; }
+    c.need.reserve(2 * (kMaxLevel + 1));
+    FMM_CUDA(cudaMemcpyAsync(c.need.p, init.data(), sizeof(int) * init.size(), cudaMemcpyHostToDevice, st));
+    FMM_LAUNCH(c, k_local_range, grid_for(ncells), 256, 0, c.cells.level.p, c.cells.begin.p, c.cells.count.p, ncells,
+               c.off, n, c.need.p, c.need.p + kMaxLevel + 1);
+    FMM_CUDA(cudaMemcpyAsync(init.data(), c.need.p, sizeof(int) * init.size(), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    c.loc_lo.assign(nlev, 0);
+    c.loc_hi.assign(nlev, 0);
+    for (int l = 0; l < nlev; ++l) {
+      if (init[kMaxLevel + 1 + l] >= 0) { c.loc_lo[l] = init[l]; c.loc_hi[l] = init[kMaxLevel + 1 + l] + 1; }
+      else { c.loc_lo[l] = c.loc_hi[l] = c.level_begin[l]; }
+    }
+  }
   int nl = 0;
   FMM_CUDA(cudaMemcpyAsync(&nl, c.scan.p + (ncells - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
   int64_t ntop = c.level_begin.size() > 2 ? c.level_begin[2] : ncells;

@@ -36,7 +36,9 @@ class fmm_stats(C.Structure):
                 ("ms_keys", C.c_double), ("ms_sort", C.c_double), ("ms_tree", C.c_double),
                 ("ms_upward", C.c_double), ("ms_traverse", C.c_double), ("ms_m2l", C.c_double),
                 ("ms_p2p", C.c_double), ("ms_downward", C.c_double), ("ms_finalize", C.c_double),
-                ("ms_set_total", C.c_double), ("ms_eval_total", C.c_double)]
+                ("ms_set_total", C.c_double), ("ms_eval_total", C.c_double),
+                ("ntot", C.c_int64), ("let_bytes_sent", C.c_int64), ("let_bytes_recv", C.c_int64),
+                ("let_cells", C.c_int64), ("let_leaves", C.c_int64), ("ms_let", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "struct_size"}
@@ -75,9 +77,10 @@ def lib():
         L.fmm_get_lists.argtypes = [vp, vp, vp]
         L.fmm_get_expansions.argtypes = [vp, vp, vp]
         L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
+        L.fmm_comm_unique_id.argtypes = [vp]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
-                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff"):
+                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
@@ -197,6 +200,14 @@ def fmm_get_expansions(ctx, order):
     return (M[..., 0] + 1j * M[..., 1]).astype(np.complex128), (L[..., 0] + 1j * L[..., 1]).astype(np.complex128)
 
 
+def fmm_comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().fmm_comm_unique_id(buf)
+    if st != FMM_OK:
+        raise FMMError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
 def fmm_eval_cutoff(ctx, rho, g):
     _check(ctx, lib().fmm_eval_cutoff(ctx, int(rho.shape[0]), _ptr(rho), _ptr(g)))
 
@@ -205,7 +216,11 @@ class FMM:
     """Owning wrapper: ``FMM(order=10, images=3, ...)``; ``set_particles(x, a, s)``;
     ``evaluate(u, s)`` writes into caller-provided float32 buffers (device or host)."""
 
-    def __init__(self, **kw):
+    def __init__(self, nccl_id: bytes = None, **kw):
+        self._id = None
+        if nccl_id is not None:
+            self._id = C.create_string_buffer(bytes(nccl_id), 128)
+            kw["nccl_id"] = C.cast(self._id, C.c_void_p)
         self.cfg = fmm_config_default(**kw)
         self.ctx = fmm_create(self.cfg)
         self.n = 0

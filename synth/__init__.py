@@ -76,3 +76,31 @@ def jittered_lattice(n: int, seed: int = 5273, lo=-np.pi, L=TWO_PI, overlap=1.0)
     xj = x.astype(np.float64) + (rng.random(x.shape) - 0.5) * 0.5 * h
     xj = np.clip(xj, lo, np.nextafter(np.float32(lo + L), np.float32(lo)))
     return xj.astype(np.float32), a, s
+
+
+# ----------------------------------------------------------------- multi-GPU --
+RANK_LATTICE = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}
+
+
+def taylor_green_rank(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
+    """Weak-scaling workload: the Taylor-Green field in
+    the fixed periodic cube [lo, lo+L)^3 sampled on a global lattice of
+    n*(mx, my, mz) points, (mx, my, mz) = RANK_LATTICE[nranks], so every rank
+    holds n^3 particles: those of its top-level Morton octants
+    [8 rank / P, 8 (rank+1) / P) (x-fastest octant bits).  P = 8 is the
+    isotropic 2n^3 lattice (C4 for n = 256); sigma = the largest spacing.
+
+    Returns (x, alpha, sigma) float32 for this rank, in x-fastest order."""
+    m = RANK_LATTICE[nranks]
+    o = 8 * rank // nranks
+    bits = (o & 1, (o >> 1) & 1, (o >> 2) & 1)
+    h = [L / (m[d] * n) for d in range(3)]
+    axes = []
+    for d in range(3):
+        i0 = bits[d] * n if m[d] == 2 else 0
+        axes.append(lo + (np.arange(i0, i0 + n, dtype=np.float64) + 0.5) * h[d])
+    Z, Y, X = np.meshgrid(axes[2], axes[1], axes[0], indexing="ij")
+    x = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=-1)
+    alpha = omega_tg(x) * (h[0] * h[1] * h[2])
+    sigma = np.full(x.shape[0], max(h))
+    return x.astype(np.float32), alpha.astype(np.float32), sigma.astype(np.float32)
