@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--images", type=int, default=3)
     ap.add_argument("--theta", default="1/2")
     ap.add_argument("--ncrit", type=int, default=64)
+    ap.add_argument("--mode", choices=["tiled", "refined"], default="tiled",
+                    help="N > 1: tiled = C5 weak scaling (one 2pi tile per GPU, reading Z27); "
+                         "refined = the fixed box refined to side*(1..2) per axis (C4 at N = 8)")
     ap.add_argument("--cpu-sample", type=int, default=32, help="oracle sample: TG n^3 lattice")
     ap.add_argument("--ref-sample", type=int, default=24, help="--impl reference sample: TG n^3 lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -206,8 +209,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     theta = theta_of(args.theta)
 
-    # C3 at N = 1; the weak-scaling blocks (synth.taylor_green_rank) at N > 1
-    x, a, s = synth.taylor_green_rank(args.side, world, rank)
+    # C3 at N = 1; the weak-scaling tiles (synth.taylor_green_tile, Z27) at N > 1
+    tiled = world > 1 and args.mode == "tiled"
+    tiles = synth.RANK_TILES[world] if tiled else (1, 1, 1)
+    x, a, s = (synth.taylor_green_tile if tiled else synth.taylor_green_rank)(args.side, world, rank)
     n = len(x)
     stream = torch.cuda.Stream()
     nccl_id = None
@@ -216,7 +221,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     f = P.FMM(order=args.order, images=args.images, theta=theta, ncrit=args.ncrit, device=local,
-              stream=stream.cuda_stream, nranks=world, rank=rank, nccl_id=nccl_id)
+              stream=stream.cuda_stream, nranks=world, rank=rank, nccl_id=nccl_id, tiles=tiles)
     with torch.cuda.stream(stream):
         xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
         ud = torch.empty((n, 3), device="cuda")
@@ -338,9 +343,13 @@ def main():
             "config": {"workload": ("C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
                                     "ncrit=%d" % (args.side, n, args.images, args.order, args.theta, args.ncrit))
                        if world == 1 else
-                       ("C5 weak scaling: Taylor-Green lattice %s in [-pi,pi)^3, %d^3 = %d particles per GPU, "
+                       ("C5 weak scaling: %s tiles of the 2pi Taylor-Green cube, one %d^3 = %d-particle tile per "
+                        "GPU, periodic k=%d, p=%d, theta=%s, ncrit=%d (reading Z27)" %
+                        ("x".join(str(m) for m in tiles), args.side, n, args.images, args.order, args.theta,
+                         args.ncrit)) if tiled else
+                       ("C4-style refinement: Taylor-Green lattice %s in [-pi,pi)^3, %d particles per GPU, "
                         "periodic k=%d, p=%d, theta=%s, ncrit=%d" %
-                        ("x".join(str(args.side * m) for m in synth.RANK_LATTICE[world]), args.side, n,
+                        ("x".join(str(args.side * m) for m in synth.RANK_LATTICE[world]), n,
                          args.images, args.order, args.theta, args.ncrit)),
                        "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
                        "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),

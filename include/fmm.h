@@ -77,6 +77,10 @@ typedef struct {
                                     (each rank passes only those, else FMM_E_ARG) */
   const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1 (all ranks
                                     pass the same id, e.g. broadcast by torch.distributed) */
+  int32_t  tiles[3];             /* periodic domain of tiles[d] cubes of side box_len per
+                                    axis (reading Z27, weak scaling); tiles[d] in {1, 2},
+                                    default (1,1,1).  With tiles != (1,1,1) rank r owns
+                                    tile/top octant r and nranks = tiles product       */
 } fmm_config;
 
 /* Per-phase device times of the last set_particles / evaluate (CUDA events on

@@ -3,6 +3,7 @@
 // per-phase CUDA-event timing, and the final combine + un-permute (a13).
 #include <cmath>
 #include <cstring>
+#include <algorithm>
 #include <new>
 
 #include "ctx.cuh"
@@ -57,6 +58,13 @@ void check_config(const fmm_config& c) {
   if (c.nranks != 1 && c.nranks != 2 && c.nranks != 4 && c.nranks != 8)
     throw FmmError(FMM_E_ARG, "nranks must be 1, 2, 4 or 8 (ranks own top-level Morton octants)");
   if (c.nranks > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "multi-GPU needs the periodic mode (images >= 1)");
+  int tp = 1;
+  for (int d = 0; d < 3; ++d) {
+    if (c.tiles[d] != 1 && c.tiles[d] != 2) throw FmmError(FMM_E_ARG, "tiles[d] must be 1 or 2");
+    tp *= c.tiles[d];
+  }
+  if (tp > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "tiles need the periodic mode");
+  if (tp > 1 && c.nranks != 1 && c.nranks != tp) throw FmmError(FMM_E_ARG, "with tiles, nranks must equal their product");
 }
 
 template <typename F>
@@ -177,6 +185,7 @@ FMM_API void fmm_config_default(fmm_config* cfg) {
   cfg->rank = 0;
   cfg->nranks = 1;
   cfg->nccl_id = nullptr;
+  cfg->tiles[0] = cfg->tiles[1] = cfg->tiles[2] = 1;
 }
 
 FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
@@ -191,6 +200,12 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     c.cfg = *cfg;
     c.P = cfg->order;
     c.nc = c.P * (c.P + 1) / 2;
+    c.tmax = 1;
+    for (int d = 0; d < 3; ++d) c.tmax = std::max(c.tmax, (int)cfg->tiles[d]);
+    for (int d = 0; d < 3; ++d) {
+      c.per[d] = cfg->tiles[d] * cfg->box_len;
+      c.per_units[d] = (1ll << 22) / c.tmax * cfg->tiles[d];
+    }
     FMM_CUDA(cudaSetDevice(cfg->device));
     if (cfg->stream) {
       c.stream = (cudaStream_t)cfg->stream;

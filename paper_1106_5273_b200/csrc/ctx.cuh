@@ -46,7 +46,10 @@ struct Ctx {
   // ---- particles and tree (set_particles) ----
   int64_t n = 0;
   bool have_particles = false;
-  double lo[3] = {0, 0, 0}, L = 1.0;
+  double lo[3] = {0, 0, 0}, L = 1.0;         // key box: the root cube
+  double per[3] = {1, 1, 1};                 // periods of the (tiled) periodic domain
+  long long per_units[3] = {1ll << 22, 1ll << 22, 1ll << 22};   // periods in half-finest-cell units
+  int tmax = 1;                              // largest tiles[d]
   DBuf<float> stage_x, stage_a, stage_s;    // host-input staging
   DBuf<float4> pos_tmp, pos, alp;           // sorted: (x,y,z,sigma), (alpha,0)
   DBuf<uint64_t> keys_tmp, keys;

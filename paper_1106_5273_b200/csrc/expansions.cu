@@ -29,7 +29,7 @@ GCells gcells(Ctx& c) {
           c.cells.parent.p, c.cells.child_begin.p, c.cells.nchild.p, c.cells.leaf.p};
 }
 
-struct Geo { double lo[3]; double L; };
+struct Geo { double lo[3]; double L; double per[3]; long long per_units[3]; int tmax; };
 
 // ---------------------------------------------------------------- P2M (a5)
 // one block per leaf; 32 particles per chunk build their R_n^m((x - c)/s)
@@ -120,7 +120,7 @@ __global__ void k_m2m(int P, int64_t first, GCells c, float2* __restrict__ M) {
 // L~_k^l(t) += (-1)^k sum_{n<p-k} sum_m M~_n^m(s) (s_s/s_t)^n I_{n+k}^{m+l}(D/s_t)
 // with D = c_t - c_s - img L evaluated exactly from integer cell coordinates.
 __global__ void k_m2l(int P, int64_t ncells, const int* __restrict__ seg_b, const int* __restrict__ seg_e,
-                      const uint64_t* __restrict__ lst, GCells c, const float2* __restrict__ M,
+                      const uint64_t* __restrict__ lst, GCells c, Geo g, const float2* __restrict__ M,
                       float2* __restrict__ Lc) {
   extern __shared__ float2 sm[];
   const int nc = P * (P + 1) / 2;
@@ -144,9 +144,9 @@ __global__ void k_m2l(int P, int64_t ncells, const int* __restrict__ seg_b, cons
     int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
     int ls = c.level[src];
     int ix = img % 3 - 1, iy = (img / 3) % 3 - 1, iz = img / 9 - 1;
-    long long dx = ctx - ((long long)(2 * c.qx[src] + 1) << (kMaxLevel - ls)) - (long long)ix * (1ll << (kMaxLevel + 1));
-    long long dy = cty - ((long long)(2 * c.qy[src] + 1) << (kMaxLevel - ls)) - (long long)iy * (1ll << (kMaxLevel + 1));
-    long long dz = ctz - ((long long)(2 * c.qz[src] + 1) << (kMaxLevel - ls)) - (long long)iz * (1ll << (kMaxLevel + 1));
+    long long dx = ctx - ((long long)(2 * c.qx[src] + 1) << (kMaxLevel - ls)) - (long long)ix * g.per_units[0];
+    long long dy = cty - ((long long)(2 * c.qy[src] + 1) << (kMaxLevel - ls)) - (long long)iy * g.per_units[1];
+    long long dz = ctz - ((long long)(2 * c.qz[src] + 1) << (kMaxLevel - ls)) - (long long)iz * g.per_units[2];
     float Dx = (float)dx * inv_st, Dy = (float)dy * inv_st, Dz = (float)dz * inv_st;
     for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
       int kk = i % nc, n, m;
@@ -182,35 +182,52 @@ __global__ void k_m2l(int P, int64_t ncells, const int* __restrict__ seg_b, cons
 
 // --------------------------------------------- periodic far layers (a8)
 // Double precision (the work is O(1) in N: 702 (k-1) M2L per far target).
-// far_M[j] holds M^{(j+1)} normalised by its side 3^j L.
-__global__ void k_far_super(int P, int k, const float2* __restrict__ Mroot, double* __restrict__ farM) {
+// far_M[j] holds M^{(j+1)} about the domain centre c0, normalised by L 3^j
+// (L = root cube side).  M^{(1)} is the root multipole shifted from the root
+// cube centre to c0 (the same point unless the domain is tiled, Z27).
+__global__ void k_far_super(int P, int k, Geo g, const float2* __restrict__ Mroot, double* __restrict__ farM) {
   extern __shared__ double smd[];
   const int nc = P * (P + 1) / 2;
   cpx<double>* R = (cpx<double>*)smd;                // [nc]
   cpx<double>* F = (cpx<double>*)farM;
+  cpx<double>* T = F + (k - 1) * 3 * nc;             // scratch: root multipole (double)
   int o = threadIdx.x;
-  for (int i = o; i < 3 * nc; i += blockDim.x) F[i] = {(double)Mroot[i].x, (double)Mroot[i].y};
-  __syncthreads();
-  for (int j = 1; j + 1 < k; ++j) {
-    const cpx<double>* Mj = F + (j - 1) * 3 * nc;
+  for (int i = o; i < 3 * nc; i += blockDim.x) T[i] = {(double)Mroot[i].x, (double)Mroot[i].y};
+  for (int j = 0; j + 1 < k; ++j) {
+    // j = 0: root (cube centre) -> c0 at the same scale; j >= 1: 27 shifted copies of M^{(j)}
+    const cpx<double>* Mj = j == 0 ? T : F + (j - 1) * 3 * nc;
     cpx<double>* Mn = F + j * 3 * nc;
     int comp = o / nc, kk0 = o % nc, n = 0, m = 0;
     if (o < 3 * nc) nm_of(kk0, n, m);
     cpx<double> acc = {0, 0};
-    for (int C3 = 0; C3 < 27; ++C3) {
+    const int ncopy = j == 0 ? 1 : 27;
+    for (int C3 = 0; C3 < ncopy; ++C3) {
       __syncthreads();
-      if (o == 0) regular_harmonics<double>((C3 % 3 - 1) / 3.0, ((C3 / 3) % 3 - 1) / 3.0, (C3 / 9 - 1) / 3.0, P, R);
+      if (o == 0) {
+        double dx, dy, dz, sc;
+        if (j == 0) {   // d = root centre - c0, in units of L
+          dx = 0.5 - 0.5 * g.per[0] / g.L; dy = 0.5 - 0.5 * g.per[1] / g.L; dz = 0.5 - 0.5 * g.per[2] / g.L;
+          sc = 1.0;
+        } else {        // d = C (.) per 3^{j-1}, in units of L 3^j
+          dx = (C3 % 3 - 1) * g.per[0] / g.L / 3.0;
+          dy = ((C3 / 3) % 3 - 1) * g.per[1] / g.L / 3.0;
+          dz = (C3 / 9 - 1) * g.per[2] / g.L / 3.0;
+          sc = 1.0 / 3.0;
+        }
+        (void)sc;
+        regular_harmonics<double>(dx, dy, dz, P, R);
+      }
       __syncthreads();
       if (o < 3 * nc) {
         for (int kk = n; kk >= 0; --kk) {
           int nn = n - kk;
-          double sc = pow(3.0, -nn);
+          double sc = j == 0 ? 1.0 : pow(3.0, -nn);
           for (int l = -kk; l <= kk; ++l) {
             int mm = m - l;
             if (mm < -nn || mm > nn) continue;
-            cpx<double> t = cmulc(cget(Mj + comp * nc, nn, mm), cget(R, kk, l));
-            acc.re += sc * t.re;
-            acc.im += sc * t.im;
+            cpx<double> t2 = cmulc(cget(Mj + comp * nc, nn, mm), cget(R, kk, l));
+            acc.re += sc * t2.re;
+            acc.im += sc * t2.im;
           }
         }
       }
@@ -224,8 +241,12 @@ __global__ void k_far_super(int P, int k, const float2* __restrict__ Mroot, doub
 // block (x = target, y = chunk): chunk = (layer j - 1) * 26 + (neighbour I != 0);
 // the 27 children C of that neighbour are summed here, the chunks are summed
 // in a fixed order by k_far_reduce (deterministic).
+// In a tiled domain (Z27) the first far layer uses the tiles' own multipoles
+// (level-1 cells, radius (sqrt3/2) box_len) instead of the elongated domain's,
+// which keeps the convergence ratio of the cubic case.
 __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, int ntg, GCells c, Geo g,
-                          const double* __restrict__ farM, double2* __restrict__ part) {
+                          const double* __restrict__ farM, int ntile, const float2* __restrict__ Mcell,
+                          double2* __restrict__ part) {
   extern __shared__ double smd[];
   const int nc = P * (P + 1) / 2;
   const int P2 = P;   // I_j for j = n + k <= p - 1
@@ -240,38 +261,62 @@ __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, int ntg
   if (I3 >= kImgCentre) ++I3;
   const int lt = c.level[t];
   const double st = g.L / (double)(1 << lt);
-  const double rx = (c.qx[t] + 0.5) * st - 0.5 * g.L, ry = (c.qy[t] + 0.5) * st - 0.5 * g.L,
-               rz = (c.qz[t] + 0.5) * st - 0.5 * g.L;   // c_t - c_0
+  const double rx = (c.qx[t] + 0.5) * st - 0.5 * g.per[0], ry = (c.qy[t] + 0.5) * st - 0.5 * g.per[1],
+               rz = (c.qz[t] + 0.5) * st - 0.5 * g.per[2];   // c_t - c_0 (domain centre)
   int kq = 0, lq = 0;
   if ((int)threadIdx.x < nc) nm_of(threadIdx.x, kq, lq);
   cpx<double> acc[3] = {{0, 0}, {0, 0}, {0, 0}};
   double scale = g.L;
   for (int jj = 1; jj < j; ++jj) scale *= 3.0;
-  const double ratio = scale / st;
-  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
-    int kk = i % nc, n, m;
-    nm_of(kk, n, m);
-    double sc = pow(ratio, n);
-    cpx<double> v = F[(j - 1) * 3 * nc + i];
-    Ms[i] = {v.re * sc, v.im * sc};
-  }
-  for (int C3 = 0; C3 < 27; ++C3) {
-    double ox = 3 * (I3 % 3 - 1) + (C3 % 3 - 1), oy = 3 * ((I3 / 3) % 3 - 1) + ((C3 / 3) % 3 - 1),
-           oz = 3 * (I3 / 9 - 1) + (C3 / 9 - 1);
-    double Dx = (rx - ox * scale) / st, Dy = (ry - oy * scale) / st, Dz = (rz - oz * scale) / st;
+  const double f3 = scale / g.L;   // 3^{j-1}
+  const bool tiled = ntile > 0 && j == 1;
+  const int nsrc = tiled ? ntile : 1;
+  for (int ts = 0; ts < nsrc; ++ts) {
+    double tox = 0, toy = 0, toz = 0;            // source centre offset from c0
     __syncthreads();
-    for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<double>(Dx, Dy, Dz, m, P2, Is);
-    __syncthreads();
-    if ((int)threadIdx.x < nc) {
-      for (int n = P - 1 - kq; n >= 0; --n)
-        for (int m = -n; m <= n; ++m) {
-          cpx<double> I = cget(Is, n + kq, m + lq);
-          for (int comp = 0; comp < 3; ++comp) {
-            cpx<double> Mv = cget(Ms + comp * nc, n, m);
-            acc[comp].re += Mv.re * I.re - Mv.im * I.im;
-            acc[comp].im += Mv.re * I.im + Mv.im * I.re;
+    if (tiled) {
+      const int tc = 1 + ts;                     // level-1 cell (a tile)
+      const double s1 = 0.5 * g.L;
+      tox = (c.qx[tc] + 0.5) * s1 - 0.5 * g.per[0];
+      toy = (c.qy[tc] + 0.5) * s1 - 0.5 * g.per[1];
+      toz = (c.qz[tc] + 0.5) * s1 - 0.5 * g.per[2];
+      const double ratio = s1 / st;
+      for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+        int kk = i % nc, n, m;
+        nm_of(kk, n, m);
+        const double sc = pow(ratio, n);
+        const float2 v = Mcell[(int64_t)tc * 3 * nc + i];
+        Ms[i] = {(double)v.x * sc, (double)v.y * sc};
+      }
+    } else {
+      const double ratio = scale / st;
+      for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+        int kk = i % nc, n, m;
+        nm_of(kk, n, m);
+        const double sc = pow(ratio, n);
+        const cpx<double> v = F[(j - 1) * 3 * nc + i];
+        Ms[i] = {v.re * sc, v.im * sc};
+      }
+    }
+    for (int C3 = 0; C3 < 27; ++C3) {
+      double ox = 3 * (I3 % 3 - 1) + (C3 % 3 - 1), oy = 3 * ((I3 / 3) % 3 - 1) + ((C3 / 3) % 3 - 1),
+             oz = 3 * (I3 / 9 - 1) + (C3 / 9 - 1);
+      double Dx = (rx - ox * g.per[0] * f3 - tox) / st, Dy = (ry - oy * g.per[1] * f3 - toy) / st,
+             Dz = (rz - oz * g.per[2] * f3 - toz) / st;
+      __syncthreads();
+      for (int m = threadIdx.x; m < P2; m += blockDim.x) irregular_column<double>(Dx, Dy, Dz, m, P2, Is);
+      __syncthreads();
+      if ((int)threadIdx.x < nc) {
+        for (int n = P - 1 - kq; n >= 0; --n)
+          for (int m = -n; m <= n; ++m) {
+            cpx<double> I = cget(Is, n + kq, m + lq);
+            for (int comp = 0; comp < 3; ++comp) {
+              cpx<double> Mv = cget(Ms + comp * nc, n, m);
+              acc[comp].re += Mv.re * I.re - Mv.im * I.im;
+              acc[comp].im += Mv.re * I.im + Mv.im * I.re;
+            }
           }
-        }
+      }
     }
   }
   if ((int)threadIdx.x < nc) {
@@ -415,7 +460,10 @@ inline int round32(int v) { return (v + 31) / 32 * 32; }
 
 }  // namespace
 
-static Geo geo(const Ctx& c) { return {{c.lo[0], c.lo[1], c.lo[2]}, c.L}; }
+static Geo geo(const Ctx& c) {
+  return {{c.lo[0], c.lo[1], c.lo[2]}, c.L, {c.per[0], c.per[1], c.per[2]},
+          {c.per_units[0], c.per_units[1], c.per_units[2]}, c.tmax};
+}
 
 void upward_pass(Ctx& c) {
   cudaStream_t st = c.stream;
@@ -434,7 +482,8 @@ void upward_pass(Ctx& c) {
     if (cnt <= 0) continue;
     FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, P, first, gc, c.M.p);
   }
-  if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc);
+  // root and level-1 cells (the tiles) are needed by every rank's far field
+  if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc * c.level_begin[2]);
 }
 
 void m2l_pass(Ctx& c) {
@@ -442,7 +491,7 @@ void m2l_pass(Ctx& c) {
   if (m2l_pass_reg(c)) return;   // register-blocked kernel (m2l.cu) for p in {4, 6, 8, 10}
   int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   size_t sm = sizeof(float2) * (nc2 + 3 * nc);
-  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), c.M.p,
+  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), geo(c), c.M.p,
                                                           c.Lc.p);
   FMM_LAUNCH_CHECK();
 }
@@ -452,31 +501,34 @@ void periodic_far_pass(Ctx& c) {
   c.far_m2l = 0;
   if (k < 2 || c.ncells == 0) return;
   int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
-  // far targets: cells at level 2 and leaves above level 2
+  // far targets: cells of side box_len / 4 (level 2 + log2 tmax) and leaves above
   // (this rank's cells only)
+  const int lt = 2 + (c.tmax == 2 ? 1 : 0);
   std::vector<int> tg;
   for (size_t i = 0; i < c.host_leaf_top.size(); ++i) {
     if (!c.host_leaf_top[i]) continue;
-    const int l = i == 0 ? 0 : 1;
-    if (c.cfg.nranks == 1 || ((int64_t)i >= c.loc_lo[l] && (int64_t)i < c.loc_hi[l])) tg.push_back((int)i);
+    int l = 0;
+    while (l + 1 < (int)c.level_begin.size() && (int64_t)i >= c.level_begin[l + 1]) ++l;
+    if ((int64_t)i >= c.loc_lo[l] && (int64_t)i < c.loc_hi[l]) tg.push_back((int)i);
   }
-  if (c.level_begin.size() > 3)
-    for (int64_t i = c.loc_lo[2]; i < c.loc_hi[2]; ++i) tg.push_back((int)i);
+  if ((int)c.level_begin.size() > lt + 1)
+    for (int64_t i = c.loc_lo[lt]; i < c.loc_hi[lt]; ++i) tg.push_back((int)i);
   if (tg.empty()) return;
-  c.far_M.reserve((size_t)(k - 1) * 3 * nc * 2);
-  FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, c.M.p, c.far_M.p);
+  c.far_M.reserve((size_t)k * 3 * nc * 2);
+  FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, geo(c), c.M.p, c.far_M.p);
   FMM_LAUNCH_CHECK();
   c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
   FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
   size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
   const int ntg = (int)tg.size(), nchunk = 26 * (k - 1);
   c.far_part.reserve((size_t)nchunk * ntg * 3 * nc);
+  const int ntile = c.tmax > 1 && c.level_begin.size() > 2 ? (int)(c.level_begin[2] - c.level_begin[1]) : 0;
   FMM_LAUNCH(c, k_far_m2l, dim3(ntg, nchunk), round32(nc), sm, P, k, c.scan.p, ntg, gcells(c), geo(c), c.far_M.p,
-             c.far_part.p);
+             ntile, c.M.p, c.far_part.p);
   FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)ntg * 3 * nc, 128), 128, 0, nc, nchunk, c.scan.p, ntg, c.far_part.p,
              c.Lc.p);
   FMM_LAUNCH_CHECK();
-  c.far_m2l = (int64_t)tg.size() * 702 * (k - 1);
+  c.far_m2l = (int64_t)tg.size() * 702 * (k - 1 + (ntile > 1 ? ntile - 1 : 0));
 }
 
 void downward_pass(Ctx& c, float* u_far, float* s_far) {

@@ -30,6 +30,7 @@ constexpr int kSub = 10;   // source subsets (x 3 components = 30 lanes)
 
 struct MCells {
   const int *level, *qx, *qy, *qz;
+  long long per[3];           // image shifts (half-finest-cell units)
 };
 
 __host__ __device__ constexpr int ci(int n, int m) { return n * (n + 1) / 2 + m; }
@@ -170,9 +171,9 @@ __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, c
         const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
         const int ls = c.level[src];
         const int ix = img % 3 - 1, iy = (img / 3) % 3 - 1, iz = img / 9 - 1;
-        const long long dx = ctx - ((long long)(2 * c.qx[src] + 1) << (kMaxLevel - ls)) - (long long)ix * (1ll << (kMaxLevel + 1));
-        const long long dy = cty - ((long long)(2 * c.qy[src] + 1) << (kMaxLevel - ls)) - (long long)iy * (1ll << (kMaxLevel + 1));
-        const long long dz = ctz - ((long long)(2 * c.qz[src] + 1) << (kMaxLevel - ls)) - (long long)iz * (1ll << (kMaxLevel + 1));
+        const long long dx = ctx - ((long long)(2 * c.qx[src] + 1) << (kMaxLevel - ls)) - (long long)ix * c.per[0];
+        const long long dy = cty - ((long long)(2 * c.qy[src] + 1) << (kMaxLevel - ls)) - (long long)iy * c.per[1];
+        const long long dz = ctz - ((long long)(2 * c.qz[src] + 1) << (kMaxLevel - ls)) - (long long)iz * c.per[2];
         dv = make_float4((float)dx * inv_st, (float)dy * inv_st, (float)dz * inv_st, 1.f);
       }
       Dsh[lane] = dv;
@@ -244,7 +245,7 @@ void launch_reg(Ctx& c) {
   size_t sm = sizeof(float4) * (size_t)kSub * D::S;
   size_t red = sizeof(float2) * (size_t)kSub * 3 * D::NC;
   if (red > sm) sm = red;
-  MCells mc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p};
+  MCells mc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, {c.per_units[0], c.per_units[1], c.per_units[2]}};
   FMM_LAUNCH(c, k_m2l_reg<P>, (unsigned)c.ncells, 32, sm, c.m2l_b.p, c.m2l_e.p, c.m2l.p, mc, c.M.p, c.Lc.p);
 }
 

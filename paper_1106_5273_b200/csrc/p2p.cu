@@ -150,6 +150,7 @@ __device__ __forceinline__ void flush(DAcc& D0, DAcc& D1, const Acc2& A) {
 __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
+                                            double px, double py, double pz,
                                             const float4* __restrict__ pos, const float4* __restrict__ alp,
                                             float* __restrict__ un, float* __restrict__ sn,
                                             unsigned long long* __restrict__ near_pairs) {
@@ -187,10 +188,10 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
       const int ls = c.level[src];
       const double ss = L / (double)(1 << ls);
       // source box centre relative to the target leaf centre, image included
-      const double ox = (c.qx[src] + 0.5) * ss + lo0 + (img % 3 - 1) * L - cx;
-      const double oy = (c.qy[src] + 0.5) * ss + lo1 + ((img / 3) % 3 - 1) * L - cy;
-      const double oz = (c.qz[src] + 0.5) * ss + lo2 + (img / 9 - 1) * L - cz;
-      const double shx = (img % 3 - 1) * L - cx, shy = ((img / 3) % 3 - 1) * L - cy, shz = (img / 9 - 1) * L - cz;
+      const double ox = (c.qx[src] + 0.5) * ss + lo0 + (img % 3 - 1) * px - cx;
+      const double oy = (c.qy[src] + 0.5) * ss + lo1 + ((img / 3) % 3 - 1) * py - cy;
+      const double oz = (c.qz[src] + 0.5) * ss + lo2 + (img / 9 - 1) * pz - cz;
+      const double shx = (img % 3 - 1) * px - cx, shy = ((img / 3) % 3 - 1) * py - cy, shz = (img / 9 - 1) * pz - cz;
       // minimum distance between the two leaf cubes
       const double hsum = 0.5 * (s + ss);
       const double gx = fmax(0.0, fabs(ox) - hsum), gy = fmax(0.0, fabs(oy) - hsum), gz = fmax(0.0, fabs(oz) - hsum);
@@ -267,7 +268,7 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
-             c.lo[2], c.L, c.pos.p, c.alp.p, u_near, s_near, c.dnear.p);
+             c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.pos.p, c.alp.p, u_near, s_near, c.dnear.p);
 }
 
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {

@@ -24,6 +24,7 @@ struct TParams {
   unsigned long long lhs_k;   // 3 * theta_den^2
   unsigned long long rhs_k;   // theta_num^2
   int leaf_first;
+  long long per[3];           // domain periods in half-finest-cell units (image shifts)
 };
 
 __device__ __forceinline__ uint64_t pack(int A, int B, int img) {
@@ -35,9 +36,9 @@ __device__ __forceinline__ uint64_t pack(int A, int B, int img) {
 __device__ __forceinline__ bool mac_accept(const TCells& c, const TParams& p, int A, int B, int img) {
   int la = c.level[A], lb = c.level[B];
   int ix = img % 3 - 1, iy = (img / 3) % 3 - 1, iz = img / 9 - 1;
-  long long dx = ((long long)(2 * c.qx[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qx[B] + 1) << (kMaxLevel - lb)) - (long long)ix * (1ll << (kMaxLevel + 1));
-  long long dy = ((long long)(2 * c.qy[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qy[B] + 1) << (kMaxLevel - lb)) - (long long)iy * (1ll << (kMaxLevel + 1));
-  long long dz = ((long long)(2 * c.qz[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qz[B] + 1) << (kMaxLevel - lb)) - (long long)iz * (1ll << (kMaxLevel + 1));
+  long long dx = ((long long)(2 * c.qx[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qx[B] + 1) << (kMaxLevel - lb)) - (long long)ix * p.per[0];
+  long long dy = ((long long)(2 * c.qy[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qy[B] + 1) << (kMaxLevel - lb)) - (long long)iy * p.per[1];
+  long long dz = ((long long)(2 * c.qz[A] + 1) << (kMaxLevel - la)) - ((long long)(2 * c.qz[B] + 1) << (kMaxLevel - lb)) - (long long)iz * p.per[2];
   unsigned long long d2 = (unsigned long long)(dx * dx) + (unsigned long long)(dy * dy) + (unsigned long long)(dz * dz);
   unsigned long long ss = (1ull << (kMaxLevel - la)) + (1ull << (kMaxLevel - lb));
   return p.lhs_k * ss * ss < p.rhs_k * d2;
@@ -143,7 +144,8 @@ void build_lists(Ctx& c) {
   TCells tc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.child_begin.p,
             c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p, c.tgt_ok.p};
   TParams tp{3ull * (unsigned long long)c.cfg.theta_den * (unsigned long long)c.cfg.theta_den,
-             (unsigned long long)c.cfg.theta_num * (unsigned long long)c.cfg.theta_num, c.cfg.traversal};
+             (unsigned long long)c.cfg.theta_num * (unsigned long long)c.cfg.theta_num, c.cfg.traversal,
+             {c.per_units[0], c.per_units[1], c.per_units[2]}};
 
   // seeds (8c-2 item 7): Interact(root, root, img) for the 27 first-layer
   // images (k >= 1) or the zero image.  The root pair never passes the MAC

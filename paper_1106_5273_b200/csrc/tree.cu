@@ -79,7 +79,7 @@ __device__ __forceinline__ int compact3(uint64_t v) {
   return (int)v;
 }
 
-struct Box { double lo[3]; double L, scale; int periodic; };
+struct Box { double lo[3]; double L, scale; double per[3]; int periodic; };
 
 // a1 wrap (periodic) + a2 keys.  Quantisation is IEEE double with explicit
 // round-to-nearest intrinsics (no FMA contraction, Z16/Z19):
@@ -92,8 +92,8 @@ __global__ void k_keys(const float* __restrict__ x, const float* __restrict__ s,
     uint64_t key = 0;
     for (int d = 0; d < 3; ++d) {
       double v = (double)x[3 * i + d];
-      if (b.periodic && (v < b.lo[d] || v >= b.lo[d] + b.L)) {
-        double w = __dsub_rn(v, __dmul_rn(b.L, floor(__ddiv_rn(__dsub_rn(v, b.lo[d]), b.L))));
+      if (b.periodic && (v < b.lo[d] || v >= b.lo[d] + b.per[d])) {
+        double w = __dsub_rn(v, __dmul_rn(b.per[d], floor(__ddiv_rn(__dsub_rn(v, b.lo[d]), b.per[d]))));
         v = (double)(float)w;
       }
       xw[d] = (float)v;
@@ -276,8 +276,8 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   Box b{};
   b.periodic = periodic;
   if (periodic) {
-    for (int d = 0; d < 3; ++d) b.lo[d] = c.cfg.box_lo[d];
-    b.L = c.cfg.box_len;
+    for (int d = 0; d < 3; ++d) { b.lo[d] = c.cfg.box_lo[d]; b.per[d] = c.per[d]; }
+    b.L = c.cfg.box_len * c.tmax;
   } else if (n > 0) {
     double ext = 0;
     for (int d = 0; d < 3; ++d) {
@@ -333,8 +333,10 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
       FMM_CUDA(cudaMemcpyAsync(&kk[1], ksorted + n - 1, 8, cudaMemcpyDeviceToHost, st));
       FMM_CUDA(cudaStreamSynchronize(st));
       const int o0 = (int)(kk[0] >> 60), o1 = (int)(kk[1] >> 60);
-      if (o0 < 8 * R / P || o1 >= 8 * (R + 1) / P)
-        throw FmmError(FMM_E_ARG, "rank holds particles outside its Morton range (octants [8r/P, 8(r+1)/P))");
+      // refined mode: octants [8r/P, 8(r+1)/P); tiled mode (Z27): octant r = tile r
+      const int olo = c.tmax > 1 ? R : 8 * R / P, ohi = c.tmax > 1 ? R + 1 : 8 * (R + 1) / P;
+      if (o0 < olo || o1 >= ohi)
+        throw FmmError(FMM_E_ARG, "rank holds particles outside its Morton range (top octants it owns)");
     }
     std::vector<int64_t> cnt = allgather_i64(c, n);
     for (int q = 0; q < P; ++q) c.rank_off[q + 1] = c.rank_off[q] + cnt[q];
@@ -437,7 +439,8 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   }
   int nl = 0;
   FMM_CUDA(cudaMemcpyAsync(&nl, c.scan.p + (ncells - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
-  int64_t ntop = c.level_begin.size() > 2 ? c.level_begin[2] : ncells;
+  const int ltop = 2 + (c.tmax == 2 ? 1 : 0);   // far-field target level (side box_len / 4)
+  int64_t ntop = (int)c.level_begin.size() > ltop ? c.level_begin[ltop] : ncells;
   c.host_leaf_top.resize(ntop);
   FMM_CUDA(cudaMemcpyAsync(c.host_leaf_top.data(), c.cells.leaf.p, sizeof(int) * ntop, cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaEventRecord(c.ev[PH_TREE], st));

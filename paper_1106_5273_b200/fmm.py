@@ -25,7 +25,7 @@ class fmm_config(C.Structure):
                 ("theta_den", C.c_int32), ("ncrit", C.c_int32), ("images", C.c_int32),
                 ("box_lo", C.c_double * 3), ("box_len", C.c_double), ("traversal", C.c_int32),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("tiles", C.c_int32 * 3)]
 
 
 class fmm_stats(C.Structure):
@@ -115,6 +115,8 @@ def fmm_config_default(**kw) -> fmm_config:
     for k, v in kw.items():
         if k == "box_lo":
             cfg.box_lo = (C.c_double * 3)(*v)
+        elif k == "tiles":
+            cfg.tiles = (C.c_int32 * 3)(*v)
         elif k == "theta":
             cfg.theta_num, cfg.theta_den = int(v[0]), int(v[1])
         else:

@@ -104,3 +104,18 @@ def taylor_green_rank(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
     alpha = omega_tg(x) * (h[0] * h[1] * h[2])
     sigma = np.full(x.shape[0], max(h))
     return x.astype(np.float32), alpha.astype(np.float32), sigma.astype(np.float32)
+
+
+RANK_TILES = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+
+def taylor_green_tile(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
+    """Weak-scaling workload of reading Z27: the periodic domain is
+    RANK_TILES[nranks] copies of the 2 pi cube and rank r holds the n^3
+    Taylor-Green lattice of tile r (tile index = the bits of r, x fastest),
+    i.e. top-level octant r of the root cube.  Per-GPU work equals the
+    single-GPU periodic run."""
+    t = (rank & 1, (rank >> 1) & 1, (rank >> 2) & 1)
+    x, a, s = taylor_green(n, 1.0, lo, L)
+    x = x.astype(np.float64) + np.array([t[0] * L, t[1] * L, t[2] * L])
+    return x.astype(np.float32), a, s

@@ -47,6 +47,7 @@ def run(fmm, x, a, s, parts=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=16)
+    ap.add_argument("--mode", choices=["tiled", "refined"], default="tiled")
     args = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -55,8 +56,10 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [P.fmm_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    x, a, s = synth.taylor_green_rank(args.side, world, rank)
-    fmm = P.FMM(images=3, nranks=world, rank=rank, device=local, nccl_id=obj[0])
+    gen = synth.taylor_green_tile if args.mode == "tiled" else synth.taylor_green_rank
+    tiles = synth.RANK_TILES[world] if args.mode == "tiled" else (1, 1, 1)
+    x, a, s = gen(args.side, world, rank)
+    fmm = P.FMM(images=3, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles)
     un, sn = run(fmm, x, a, s, parts=1)
     u, st = run(fmm, x, a, s)
     p2p, m2l = P.fmm_get_lists(fmm.ctx)
@@ -66,11 +69,11 @@ def main():
     dist.all_gather_object(gathered, dict(u=u, s=st, un=un, sn=sn, p2p=p2p, m2l=m2l, n=len(x), stats=stats))
     ok, msg = True, {}
     if rank == 0:
-        blocks = [synth.taylor_green_rank(args.side, world, r) for r in range(world)]
+        blocks = [gen(args.side, world, r) for r in range(world)]
         X = np.concatenate([b[0] for b in blocks])
         A = np.concatenate([b[1] for b in blocks])
         S = np.concatenate([b[2] for b in blocks])
-        single = P.FMM(images=3, device=local)
+        single = P.FMM(images=3, device=local, tiles=tiles)
         Un, Sn = run(single, X, A, S, parts=1)
         U, SS = run(single, X, A, S)
         gp2p, gm2l = P.fmm_get_lists(single.ctx)
@@ -103,6 +106,7 @@ def main():
                                                    "ms_let")} for g in gathered]
         msg["ok"] = bool(ok)
         msg["world"] = world
+        msg["mode"] = args.mode
         print(json.dumps(msg), flush=True)
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(okt, src=0)

@@ -18,13 +18,14 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("mode", ["tiled", "refined"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_distributed_equals_single_gpu(world):
+def test_distributed_equals_single_gpu(world, mode):
     if _ngpu() < world:
         pytest.skip("needs %d GPUs" % world)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
-           os.path.join(ROOT, "tests", "mgpu_check.py"), "--side", "16"]
+           os.path.join(ROOT, "tests", "mgpu_check.py"), "--side", "16", "--mode", mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
