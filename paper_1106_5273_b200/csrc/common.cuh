@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "../../include/fmm.h"
 
@@ -158,5 +159,16 @@ __device__ void irregular_column(T x, T y, T z, int m, int P2, cpx<T>* I) {
     a = v;
   }
 }
+
+// compile-time loop: f(integral_constant<int, i>) for i = B, B+S, ... (excluding E)
+template <int B, int E, int S, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr ((S > 0 && B < E) || (S < 0 && B > E)) {
+    f(std::integral_constant<int, B>{});
+    sfor<B + S, E, S>(f);
+  }
+}
+
+__host__ __device__ constexpr int ci(int n, int m) { return n * (n + 1) / 2 + m; }
 
 }  // namespace fmmb

@@ -94,6 +94,7 @@ void build_lists(Ctx& c);
 void upward_pass(Ctx& c);
 void m2l_pass(Ctx& c);
 bool m2l_pass_reg(Ctx& c);
+bool l2p_pass_reg(Ctx& c, float* u_far, float* s_far);
 void comm_init(Ctx& c);
 void comm_unique_id(void* out);
 void comm_destroy(Ctx& c);

@@ -542,7 +542,7 @@ void downward_pass(Ctx& c, float* u_far, float* s_far) {
     FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, c.Lc.p);
     FMM_LAUNCH_CHECK();
   }
-  if (c.nleaves > 0) {
+  if (c.nleaves > 0 && !l2p_pass_reg(c, u_far, s_far)) {
     size_t sm = sizeof(float2) * (3 * nc + 32 * nc);
     FMM_LAUNCH(c, k_l2p, (unsigned)c.nleaves, 32, sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.Lc.p, u_far, s_far);
     FMM_LAUNCH_CHECK();

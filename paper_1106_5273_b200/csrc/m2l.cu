@@ -33,7 +33,6 @@ struct MCells {
   long long per[3];           // image shifts (half-finest-cell units)
 };
 
-__host__ __device__ constexpr int ci(int n, int m) { return n * (n + 1) / 2 + m; }
 
 template <int P>
 struct Dims {
@@ -50,15 +49,6 @@ struct Dims {
 __device__ __forceinline__ void cmac2(float2& acc, float a, float b, float2 B, float2 Bp) {
   acc = __ffma2_rn(make_float2(a, a), B, acc);
   acc = __ffma2_rn(make_float2(b, b), Bp, acc);
-}
-
-// compile-time loop: f(integral_constant<int, i>) for i = B, B+S, ... (excluding E)
-template <int B, int E, int S, typename F>
-__device__ __forceinline__ void sfor(F&& f) {
-  if constexpr ((S > 0 && B < E) || (S < 0 && B > E)) {
-    f(std::integral_constant<int, B>{});
-    sfor<B + S, E, S>(f);
-  }
 }
 
 // Is holds, per (j, mp): Is[2 ci] = (Re I, Im I, -Im I, Re I) of I_j^mp and
