@@ -56,13 +56,26 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // g(rho) of Eq. 2 from rho, x = rho^2, e = exp(-rho^2): the two pieces.
 //   series: g = rho^3 sum_k a_k x^k               (accurate as rho -> 0; used for x < 0.64)
 //   erfcx : g = 1 - e (h(t) + (2/sqrt pi) rho),  h ~ erfcx, t = 1/(1 + rho/2)
-__device__ __forceinline__ float2 series_g(float2 rho, float2 x) {
+// s(x) = g / rho^3 = (4/sqrt pi) sum_n (-x)^n / (n! (2n+3))
+__device__ __forceinline__ float2 series_s(float2 x) {
   float2 s = make_float2(2.945851975e-06f, 2.945851975e-06f);
   const float a[8] = {-2.633938311e-05f, 2.089590998e-04f, -1.446640003e-03f, 8.548326790e-03f,
                       -4.179182276e-02f, 1.611970216e-01f, -4.513516724e-01f, 7.522527575e-01f};
 #pragma unroll
   for (int k = 0; k < 8; ++k) s = __ffma2_rn(s, x, make_float2(a[k], a[k]));
-  return __fmul2_rn(s, __fmul2_rn(rho, x));
+  return s;
+}
+// T(x) = ((4/sqrt pi) e^{-x} - 3 s(x)) / x = (4/sqrt pi) sum_m (-1)^{m+1} 2(m+1) x^m / ((m+1)! (2m+5))
+__device__ __forceinline__ float2 series_t(float2 x) {
+  float2 s = make_float2(5.407844333e-07f, 5.407844333e-07f);
+  const float a[9] = {-5.330589414e-06f, 4.713363271e-05f, -3.687513618e-04f, 2.507509260e-03f, -1.446639958e-02f,
+                      6.838661619e-02f, -2.507509260e-01f, 6.447880955e-01f, -9.027033337e-01f};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) s = __ffma2_rn(s, x, make_float2(a[k], a[k]));
+  return s;
+}
+__device__ __forceinline__ float2 series_g(float2 rho, float2 x) {
+  return __fmul2_rn(series_s(x), __fmul2_rn(rho, x));
 }
 __device__ __forceinline__ float2 erfcx_g(float2 rho, float2 e) {
   const float2 d = __ffma2_rn(make_float2(0.5f, 0.5f), rho, make_float2(1.f, 1.f));
@@ -112,15 +125,22 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
     const float2 ea = __fmul2_rn(x, bc(-1.4426950408889634f));
     const float2 e = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
     const float2 rho = __fmul2_rn(__fmul2_rn(r2, inv), bc(a.w));
-    float2 g = erfcx_g(rho, e);
-    // series piece only when some lane has a close pair (warp-uniform branch)
-    if (__any_sync(0xffffffffu, fminf(x.x, x.y) < 0.64f)) {
-      const float2 gs = series_g(rho, x);
-      g = make_float2(x.x < 0.64f ? gs.x : g.x, x.y < 0.64f ? gs.y : g.y);
-    }
+    const float2 g = erfcx_g(rho, e);
     f = __fmul2_rn(g, inv3);
     const float2 t1 = __fmul2_rn(__fmul2_rn(rho, x), bc(2.2567583341910252f));   // (4/sqrt pi) rho^3
     fp = __fmul2_rn(__ffma2_rn(t1, e, __fmul2_rn(g, bc(-3.0f))), __fmul2_rn(inv3, inv2));
+    // close pairs (rho < 0.8, evaluated only when some lane of the warp has
+    // one): f = g/r^3 and f'/r from the Taylor series in x = rho^2 without
+    // dividing by r, so they stay exact as r -> 0 (r = 0 still contributes 0, Z7):
+    //   f = k^{3/2} s(x),  f'/r = k^{5/2} T(x),  k = 1/(2 sigma^2)
+    if (__any_sync(0xffffffffu, fminf(x.x, x.y) < 0.64f)) {
+      const float2 sx = series_s(x), tx = series_t(x);
+      const float kk = -q.w, k32 = kk * a.w, k52 = kk * k32;
+      f = make_float2(x.x < 0.64f ? (r2.x > 0.f ? k32 * sx.x : 0.f) : f.x,
+                      x.y < 0.64f ? (r2.y > 0.f ? k32 * sx.y : 0.f) : f.y);
+      fp = make_float2(x.x < 0.64f ? (r2.x > 0.f ? k52 * tx.x : 0.f) : fp.x,
+                       x.y < 0.64f ? (r2.y > 0.f ? k52 * tx.y : 0.f) : fp.y);
+    }
   } else {
     f = inv3;
     fp = __fmul2_rn(__fmul2_rn(inv3, inv2), bc(-3.0f));
