@@ -53,9 +53,10 @@ def parse():
     ap.add_argument("--images", type=int, default=3)
     ap.add_argument("--theta", default="1/2")
     ap.add_argument("--ncrit", type=int, default=64)
-    ap.add_argument("--mode", choices=["tiled", "refined"], default="tiled",
-                    help="N > 1: tiled = C5 weak scaling (one 2pi tile per GPU, reading Z27); "
-                         "refined = the fixed box refined to side*(1..2) per axis (C4 at N = 8)")
+    ap.add_argument("--mode", choices=["tiled", "refined", "strong"], default="tiled",
+                    help="N > 1: tiled = C5 weak scaling (one 2pi tile of side^3 per GPU, reading Z27); "
+                         "refined = the fixed box refined to side*(1..2) per axis; "
+                         "strong = C4: one side^3 lattice split over the GPUs by Morton octants")
     ap.add_argument("--cpu-sample", type=int, default=32, help="oracle sample: TG n^3 lattice")
     ap.add_argument("--ref-sample", type=int, default=24, help="--impl reference sample: TG n^3 lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -212,7 +213,9 @@ def main():
     # C3 at N = 1; the weak-scaling tiles (synth.taylor_green_tile, Z27) at N > 1
     tiled = world > 1 and args.mode == "tiled"
     tiles = synth.RANK_TILES[world] if tiled else (1, 1, 1)
-    x, a, s = (synth.taylor_green_tile if tiled else synth.taylor_green_rank)(args.side, world, rank)
+    gen = {"tiled": synth.taylor_green_tile, "refined": synth.taylor_green_rank,
+           "strong": synth.taylor_green_octants}[args.mode]
+    x, a, s = gen(args.side, world, rank)
     n = len(x)
     stream = torch.cuda.Stream()
     nccl_id = None
@@ -338,7 +341,8 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "s_per_step": ms_max / 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if (world > 1 and args.mode == "strong") else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic Taylor-Green lattice (reading Z26), generated on host, resident in HBM",
             "config": {"workload": ("C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
                                     "ncrit=%d" % (args.side, n, args.images, args.order, args.theta, args.ncrit))
@@ -350,7 +354,10 @@ def main():
                        ("C4-style refinement: Taylor-Green lattice %s in [-pi,pi)^3, %d particles per GPU, "
                         "periodic k=%d, p=%d, theta=%s, ncrit=%d" %
                         ("x".join(str(args.side * m) for m in synth.RANK_LATTICE[world]), n,
-                         args.images, args.order, args.theta, args.ncrit)),
+                         args.images, args.order, args.theta, args.ncrit)) if args.mode == "refined" else
+                       ("C4 strong scaling: Taylor-Green %d^3 in [-pi,pi)^3 split by Morton octants, %d particles on "
+                        "this GPU, periodic k=%d, p=%d, theta=%s, ncrit=%d" %
+                        (args.side, n, args.images, args.order, args.theta, args.ncrit)),
                        "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
                        "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),
                        "parallelism": "1 GPU" if world == 1 else

@@ -119,3 +119,14 @@ def taylor_green_tile(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
     x, a, s = taylor_green(n, 1.0, lo, L)
     x = x.astype(np.float64) + np.array([t[0] * L, t[1] * L, t[2] * L])
     return x.astype(np.float32), a, s
+
+
+def taylor_green_octants(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
+    """Strong-scaling workload (C4: n^3 in the fixed periodic cube): rank r
+    holds the lattice points of top-level Morton octants [8r/P, 8(r+1)/P)
+    (z halves for P = 2, y-z quarters for P = 4, octants for P = 8)."""
+    x, a, s = taylor_green(n, 1.0, lo, L)
+    mid = lo + 0.5 * L
+    o = ((x[:, 0] >= mid).astype(int) | ((x[:, 1] >= mid).astype(int) << 1) | ((x[:, 2] >= mid).astype(int) << 2))
+    keep = (o >= 8 * rank // nranks) & (o < 8 * (rank + 1) // nranks)
+    return x[keep], a[keep], s[keep]
