@@ -376,6 +376,7 @@ FMM_API fmm_status fmm_get_lists(fmm_ctx* h, int64_t* p2p, int64_t* m2l) {
       if (!out || n == 0) return;
       std::vector<uint64_t> v(n);
       FMM_CUDA(cudaMemcpy(v.data(), L.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+      std::sort(v.begin(), v.end());   // canonical (target, source, image) order (Z20)
       for (int64_t i = 0; i < n; ++i) {
         out[3 * i] = (int64_t)(v[i] >> 32);
         out[3 * i + 1] = (int64_t)((v[i] >> 5) & 0x7ffffff);

@@ -122,13 +122,16 @@ void exclusive_scan(Ctx& c, const int* in, int* out, int64_t n) {
   });
 }
 
-void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n) {
+// begin_bit = 0: the canonical (target, source, image) order; begin_bit = 32:
+// grouped by target only, stable, i.e. the traversal's (deterministic)
+// emission order within a target
+void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
   if (n <= 1) return;
   c.sort_tmp.reserve(n);
   uint64_t* in = lst.p;
   uint64_t* out = c.sort_tmp.p;
   cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, 0, 59, c.stream);
+    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, begin_bit, 59, c.stream);
   });
   std::swap(lst.p, c.sort_tmp.p);
   std::swap(lst.cap, c.sort_tmp.cap);
@@ -202,9 +205,11 @@ void build_lists(Ctx& c) {
     nf = add_q;
   }
 
-  // canonical order + per-target segments
+  // per-target segments: P2P in canonical order (it fixes the near-field
+  // summation order, identical on 1 and N GPUs), M2L grouped by target only
+  // (half the radix passes; fmm_get_lists returns the canonical order)
   sort_list(c, c.p2p, c.np2p);
-  sort_list(c, c.m2l, c.nm2l);
+  sort_list(c, c.m2l, c.nm2l, 32);
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
   c.m2l_b.reserve(c.ncells); c.m2l_e.reserve(c.ncells);
   FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
