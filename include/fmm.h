@@ -153,6 +153,15 @@ fmm_status fmm_get_lists(fmm_ctx* ctx, int64_t* p2p, int64_t* m2l);
  * (interleaved re, im) -- either pointer may be NULL. */
 fmm_status fmm_get_expansions(const fmm_ctx* ctx, float* M, float* L);
 
+/* NEXT-1: one vortex-method time step around the evaluation:
+ * midpoint RK2 -- (u1, s1) = FMM(x, alpha, sigma); x_h = x + dt/2 u1,
+ * alpha_h = alpha + dt/2 s1, sigma_h^2 = sigma^2 + nu dt; (u2, s2) =
+ * FMM(x_h, alpha_h, sigma_h); x += dt u2, alpha += dt s2, sigma^2 += 2 nu dt
+ * (Eq. 4, exact).  x[n][3], alpha[n][3], sigma[n] are read and overwritten
+ * (host or device).  Single GPU in this build.  Errors: FMM_E_ARG, plus those
+ * of set_particles / evaluate. */
+fmm_status fmm_step(fmm_ctx* ctx, int64_t n, float* x, float* alpha, float* sigma, double dt, double nu);
+
 /* Multi-GPU bootstrap: writes a fresh 128-byte ncclUniqueId into id (one rank
  * calls it and broadcasts the bytes to the others, e.g. via torch.distributed;
  * every rank then passes them as fmm_config.nccl_id).  Errors: FMM_E_NCCL. */

@@ -285,3 +285,17 @@ def rel_l2(a, b) -> float:
     a = np.asarray(a, dtype=np.float64); b = np.asarray(b, dtype=np.float64)
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a - b))
+
+
+# ------------------------------------------------------- NEXT-1 time step --
+def rk2_step(x, alpha, sigma, dt, nu=0.0, images=0, box_len=2 * np.pi):
+    """Midpoint RK2 of P:69 / Eq. 4 with the c-1 direct sum as the right-hand
+    side: x' = x + dt u(t+dt/2), alpha' = alpha + dt dalpha/dt(t+dt/2),
+    sigma'^2 = sigma^2 + 2 nu dt.  Returns float64 arrays."""
+    x = _c64(x); alpha = _c64(alpha); sigma = _c64(sigma)
+    u1, s1 = direct(x, alpha, x, alpha, sigma, box_len, images)
+    xh = x + 0.5 * dt * u1
+    ah = alpha + 0.5 * dt * s1
+    sh = np.sqrt(sigma ** 2 + nu * dt)
+    u2, s2 = direct(xh, ah, xh, ah, sh, box_len, images)
+    return x + dt * u2, alpha + dt * s2, np.sqrt(sigma ** 2 + 2 * nu * dt)

@@ -427,3 +427,41 @@ FMM_API fmm_status fmm_comm_unique_id(void* id) {
     return FMM_E_INTERNAL;
   }
 }
+
+FMM_API fmm_status fmm_step(fmm_ctx* h, int64_t n, float* x, float* alpha, float* sigma, double dt, double nu) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (n < 0 || (n > 0 && (!x || !alpha || !sigma))) throw FmmError(FMM_E_ARG, "bad arguments");
+    if (!(dt > 0.0) || !(nu >= 0.0) || !std::isfinite(dt) || !std::isfinite(nu)) throw FmmError(FMM_E_ARG, "need dt > 0, nu >= 0");
+    if (c.cfg.nranks > 1) throw FmmError(FMM_E_ARG, "fmm_step is single-GPU in this build (no particle migration)");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    cudaStream_t st = c.stream;
+    c.st_x.reserve(3 * n); c.st_a.reserve(3 * n); c.st_s.reserve(n);
+    c.st_u.reserve(3 * n); c.st_da.reserve(3 * n);
+    c.st_xh.reserve(3 * n); c.st_ah.reserve(3 * n); c.st_sh.reserve(n);
+    if (n > 0) {
+      FMM_CUDA(cudaMemcpyAsync(c.st_x.p, x, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(c.st_a.p, alpha, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(c.st_s.p, sigma, sizeof(float) * n, cudaMemcpyDefault, st));
+    }
+    // stage 1 at t
+    set_particles_impl(c, n, c.st_x.p, c.st_a.p, c.st_s.p);
+    evaluate_impl(c, 3, c.st_u.p, c.st_da.p);
+    step_stage_update(c, c.st_x.p, c.st_a.p, c.st_s.p, c.st_u.p, c.st_da.p, n, 0.5 * dt, nu * dt, c.st_xh.p,
+                      c.st_ah.p, c.st_sh.p);
+    // stage 2 at t + dt/2
+    set_particles_impl(c, n, c.st_xh.p, c.st_ah.p, c.st_sh.p);
+    evaluate_impl(c, 3, c.st_u.p, c.st_da.p);
+    // x' = x + dt u(t+dt/2), alpha' = alpha + dt dalpha/dt(t+dt/2), sigma'^2 = sigma^2 + 2 nu dt (Eq. 4)
+    step_stage_update(c, c.st_x.p, c.st_a.p, c.st_s.p, c.st_u.p, c.st_da.p, n, dt, 2.0 * nu * dt, c.st_xh.p,
+                      c.st_ah.p, c.st_sh.p);
+    if (n > 0) {
+      FMM_CUDA(cudaMemcpyAsync(x, c.st_xh.p, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(alpha, c.st_ah.p, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(sigma, c.st_sh.p, sizeof(float) * n, cudaMemcpyDefault, st));
+    }
+    FMM_CUDA(cudaStreamSynchronize(st));
+  });
+}

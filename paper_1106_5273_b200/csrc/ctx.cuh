@@ -83,6 +83,9 @@ struct Ctx {
   // ---- counters ----
   int64_t launches = 0, cub_calls = 0;       // since the last set_particles
 
+  // ---- time step (NEXT-1) ----
+  DBuf<float> st_x, st_a, st_s, st_u, st_da, st_xh, st_ah, st_sh;
+
   // ---- timing ----
   cudaEvent_t ev[PH_N + 1] = {};
   fmm_stats stats{};
@@ -104,6 +107,8 @@ void alltoallv_bytes(Ctx& c, const void* sbuf, const std::vector<int64_t>& soff,
                      void* rbuf, const std::vector<int64_t>& roff, const std::vector<int64_t>& rbytes);
 void allreduce_sum_f32(Ctx& c, float* p, int64_t n);
 void let_exchange(Ctx& c);
+void step_stage_update(Ctx& c, const float* x, const float* a, const float* s, const float* u, const float* da,
+                       int64_t n, double h, double two_nu_t, float* xo, float* ao, float* so);
 void periodic_far_pass(Ctx& c);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);

@@ -78,9 +78,10 @@ def lib():
         L.fmm_get_expansions.argtypes = [vp, vp, vp]
         L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
         L.fmm_comm_unique_id.argtypes = [vp]
+        L.fmm_step.argtypes = [vp, i64, vp, vp, vp, C.c_double, C.c_double]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
-                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id"):
+                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id", "fmm_step"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
@@ -202,6 +203,10 @@ def fmm_get_expansions(ctx, order):
     return (M[..., 0] + 1j * M[..., 1]).astype(np.complex128), (L[..., 0] + 1j * L[..., 1]).astype(np.complex128)
 
 
+def fmm_step(ctx, n, x, alpha, sigma, dt, nu):
+    _check(ctx, lib().fmm_step(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), float(dt), float(nu)))
+
+
 def fmm_comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     st = lib().fmm_comm_unique_id(buf)
@@ -233,6 +238,11 @@ class FMM:
 
     def evaluate(self, u, dalpha_dt, parts=3):
         fmm_evaluate_parts(self.ctx, parts, u, dalpha_dt)
+
+    def step(self, x, alpha, sigma, dt, nu=0.0):
+        """One midpoint-RK2 vortex step (NEXT-1); overwrites x, alpha, sigma."""
+        fmm_step(self.ctx, x.shape[0], x, alpha, sigma, dt, nu)
+        self.n = int(x.shape[0])
 
     def stats(self):
         return fmm_get_stats(self.ctx)
