@@ -311,22 +311,30 @@ def main():
 
     if rank == 0:
         traffic, prof = load_profile_traffic()
-        from tools.sass_flops import p2p_flops_per_pair
+        from tools.sass_flops import p2p_flops_per_pair, sass_digest
         fpp = p2p_flops_per_pair(P.fmm.LIB_PATH)
         near = statistics.mean(st["p2p_near_pairs"] for st in stats)
         hw_flops = near * fpp.get("near", 0.0) + (pairs - near) * fpp.get("far", 0.0)
+        flops_src = "static SASS count (tools/sass_flops.py)"
+        # prefer the ncu-counted flops of this exact build on this exact workload
+        if prof and prof.get("hw_flops_ncu") and prof.get("hw_flops_ncu_pairs") == pairs and \
+                prof.get("sass_sha1") == sass_digest(P.fmm.LIB_PATH):
+            hw_flops = prof["hw_flops_ncu"]
+            flops_src = "ncu sm__sass_thread_inst_executed_op_{fadd,fmul,ffma,fadd2,fmul2,ffma2}_pred_on " \
+                        "(same SASS, same workload; profiles/latest_p2p.json)"
         t_p2p = phase["ms_p2p"] * 1e-3
         achieved = hw_flops / t_p2p / 1e12
         roof = {"kernel": "k_p2p (near field, a12)", "bound": "alu", "achieved": achieved,
                 "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
                 "traffic": traffic,
                 "per_launch": {"ms": phase["ms_p2p"], "pairs": pairs, "near_pairs": int(near),
-                               "hw_flops_per_pair": fpp, "hw_flops": hw_flops},
+                               "hw_flops_per_pair_static": fpp, "hw_flops": hw_flops,
+                               "hw_flops_per_pair": hw_flops / pairs if pairs else None, "hw_flops_source": flops_src},
                 "model": {"flops_per_pair": FLOPS_PER_PAIR,
                           "achieved_tflops": FLOPS_PER_PAIR * pairs / t_p2p / 1e12,
                           "note": "paper-style Table 1 count (sqrt/rsqrt/exp/div = 1 flop); not a hardware rate"},
-                "note": "achieved = FP32 FADD/FMUL (1) + FFMA (2) per pair counted from the kernel's SASS "
-                        "(tools/sass_flops.py; packed FP32x2 ops count per lane) x pairs on each tile kind / "
+                "note": "achieved = hardware FP32 flops of one P2P launch (FADD/FMUL 1, FFMA 2, packed FP32x2 "
+                        "ops per lane; source in per_launch.hw_flops_source) / "
                         "mean P2P launch time (CUDA events on the launch stream); peak = 148 SM x 128 FP32 lanes "
                         "x 2 x 1.965 GHz (derived, DESIGN.md; FFMA/FFMA2 probe measured 72.4/73.9 TFLOP/s)"}
         if prof:

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
   const double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s,
                cz = lo2 + (c.qz[leaf] + 0.5) * s;
   const int eb = seg_b[leaf], ee = seg_e[leaf];
+  const float hst = (float)(0.5 * s);
   unsigned long long nnear = 0;                   // pairs evaluated with the regularised kernel
   for (int t0 = 0; t0 < tcnt; t0 += TP) {
     const int i0 = t0 + lane, i1 = t0 + lane + NT;
@@ -205,51 +206,55 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
     for (int e = eb; e < ee; ++e) {
       const uint64_t ent = lst[e];
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
-      const int ls = c.level[src];
-      const double ss = L / (double)(1 << ls);
-      // source box centre relative to the target leaf centre, image included
-      const double ox = (c.qx[src] + 0.5) * ss + lo0 + (img % 3 - 1) * px - cx;
-      const double oy = (c.qy[src] + 0.5) * ss + lo1 + ((img / 3) % 3 - 1) * py - cy;
-      const double oz = (c.qz[src] + 0.5) * ss + lo2 + (img / 9 - 1) * pz - cz;
+      // image shift minus the target leaf centre: sources land in the target frame
       const double shx = (img % 3 - 1) * px - cx, shy = ((img / 3) % 3 - 1) * py - cy, shz = (img / 9 - 1) * pz - cz;
-      // minimum distance between the two leaf cubes
-      const double hsum = 0.5 * (s + ss);
-      const double gx = fmax(0.0, fabs(ox) - hsum), gy = fmax(0.0, fabs(oy) - hsum), gz = fmax(0.0, fabs(oz) - hsum);
-      const float dmin2 = (float)(gx * gx + gy * gy + gz * gz);
       const int sb = c.begin[src], scnt = c.count[src];
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
-        float smax = 0.f;
+        // stage the tile, far sources first: a source is "far" when it is
+        // >= 4.5 sqrt2 sigma_j from the whole target leaf cube, so every pair
+        // it forms has rho >= 4.5 (then 1 - g < 1e-8: the exact singular branch)
+        float4 qv[2], av[2];
+        bool fj[2], vj[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int j = s0 + lane + h * NT;
-          if (j < scnt) {
+          vj[h] = j < scnt;
+          fj[h] = false;
+          if (vj[h]) {
             const float4 p = pos[sb + j];
             const float4 a = alp[sb + j];
             const float w = 1.0f / (2.0f * p.w * p.w);
-            sx[lane + h * NT] = make_float4((float)((double)p.x + shx), (float)((double)p.y + shy),
-                                            (float)((double)p.z + shz), -w);
-            sa[lane + h * NT] = make_float4(a.x * k4, a.y * k4, a.z * k4, sqrtf(w));
-            smax = fmaxf(smax, p.w);
+            const float qx = (float)((double)p.x + shx), qy = (float)((double)p.y + shy), qz = (float)((double)p.z + shz);
+            qv[h] = make_float4(qx, qy, qz, -w);
+            av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, sqrtf(w));
+            const float gx = fmaxf(0.f, fabsf(qx) - hst), gy = fmaxf(0.f, fabsf(qy) - hst), gz = fmaxf(0.f, fabsf(qz) - hst);
+            fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
           }
         }
-        for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned f0 = __ballot_sync(0xffffffffu, fj[0]), f1 = __ballot_sync(0xffffffffu, fj[1]);
+        const unsigned n0 = __ballot_sync(0xffffffffu, vj[0] && !fj[0]), n1 = __ballot_sync(0xffffffffu, vj[1] && !fj[1]);
+        const int nfar = __popc(f0) + __popc(f1);
+        const int nj = nfar + __popc(n0) + __popc(n1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!vj[h]) continue;
+          const int dst = fj[h] ? (h == 0 ? __popc(f0 & lt) : __popc(f0) + __popc(f1 & lt))
+                                : nfar + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
+          sx[dst] = qv[h];
+          sa[dst] = av[h];
+        }
         __syncwarp();
-        const int nj = min(TP, scnt - s0);
-        // every pair of this tile has rho >= 4.5 => exact singular branch
-        const bool far = dmin2 >= 40.5f * smax * smax;
-        if (!far) nnear += (unsigned long long)nj * (unsigned long long)min(TP, tcnt - t0);
+        nnear += (unsigned long long)(nj - nfar) * (unsigned long long)min(TP, tcnt - t0);
         Acc2 A;
         zero(A);
         const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
         const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
-        if (far) {
 #pragma unroll 4
-          for (int jj = 0; jj < nj; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
-        } else {
+        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
 #pragma unroll 2
-          for (int jj = 0; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
-        }
+        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
         flush(D0, D1, A);
       }
     }

@@ -89,3 +89,12 @@ if __name__ == "__main__":
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     print(p2p_flops_per_pair(sys.argv[1] if len(sys.argv) > 1 else
                              os.path.join(root, "paper_1106_5273_b200", "libfmm_b200.so")))
+
+
+def sass_digest(lib, func_regex="k_p2p"):
+    """sha1 of a kernel's SASS: ties an ncu flop count to the exact build."""
+    import hashlib
+    h = hashlib.sha1()
+    for _, t in _sass(lib, func_regex):
+        h.update(t.encode())
+    return h.hexdigest()
