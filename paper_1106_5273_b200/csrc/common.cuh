@@ -2,6 +2,7 @@
 // (No code here is shared with oracle/: the oracle is an independent program.)
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include <stdexcept>

@@ -44,13 +44,6 @@ struct Dims {
   static constexpr int S = 2 * NC2 + ((7 - (2 * NC2) % 8) + 8) % 8;
 };
 
-// acc += a * B + b * B' with scalar a, b broadcast into both FP32 lanes:
-// two FFMA2 (packed FP32x2 FMA, sm_100a) per complex multiply-add.
-__device__ __forceinline__ void cmac2(float2& acc, float a, float b, float2 B, float2 Bp) {
-  acc = __ffma2_rn(make_float2(a, a), B, acc);
-  acc = __ffma2_rn(make_float2(b, b), Bp, acc);
-}
-
 // Is holds, per (j, mp): Is[2 ci] = (Re I, Im I, -Im I, Re I) of I_j^mp and
 // Is[2 ci + 1] the same for I_j^{-mp} = (-1)^mp conj(I_j^mp).  For a complex
 // M = (ar, ai):  M * I = ar (Re I, Im I) + ai (-Im I, Re I).
@@ -69,26 +62,36 @@ __device__ __forceinline__ void m2l_accumulate(const float4* __restrict__ Is, co
         Cp = make_float2(in.x, in.y);
         Cq = make_float2(in.z, in.w);
       }
-      sfor<0, j + 1, 1>([&](auto Nc) {
-        constexpr int n = decltype(Nc)::value;
-        constexpr int k = j - n;
-        sfor<0, k + 1, 1>([&](auto Lc_) {
-          constexpr int l = decltype(Lc_)::value;
-          constexpr int o = ci(k, l);
-          constexpr int m1 = mp - l;               // term with I_j^{+mp}
-          if constexpr (m1 >= -n && m1 <= n) {
-            if constexpr (m1 >= 0) {
-              cmac2(L[o], Mr[ci(n, m1)], Mi[ci(n, m1)], Bp, Bq);
+      // four passes over the (n, l) targets of this I_j^{mp}: each pass issues
+      // one FFMA2 per local coefficient, so consecutive FFMA2s are independent
+      // (a single pass would chain four dependent FFMA2s on the same L[o])
+      sfor<0, 4, 1>([&](auto PSc) {
+        constexpr int ps = decltype(PSc)::value;
+        sfor<0, j + 1, 1>([&](auto Nc) {
+          constexpr int n = decltype(Nc)::value;
+          constexpr int k = j - n;
+          sfor<0, k + 1, 1>([&](auto Lc_) {
+            constexpr int l = decltype(Lc_)::value;
+            constexpr int o = ci(k, l);
+            if constexpr (ps < 2) {
+              constexpr int m1 = mp - l;             // term with I_j^{+mp}
+              if constexpr (m1 >= -n && m1 <= n) {
+                constexpr int ma = m1 >= 0 ? m1 : -m1;
+                constexpr float s = (m1 < 0 && (ma & 1)) ? -1.f : 1.f;   // M_n^m = (-1)^m conj(M_n^{-m})
+                constexpr float si = m1 < 0 ? -s : s;
+                if constexpr (ps == 0) L[o] = __ffma2_rn(make_float2(s * Mr[ci(n, ma)], s * Mr[ci(n, ma)]), Bp, L[o]);
+                else L[o] = __ffma2_rn(make_float2(si * Mi[ci(n, ma)], si * Mi[ci(n, ma)]), Bq, L[o]);
+              }
             } else {
-              constexpr float s = ((-m1) & 1) ? -1.f : 1.f;   // M_n^m = s conj(M_n^{-m})
-              cmac2(L[o], s * Mr[ci(n, -m1)], -s * Mi[ci(n, -m1)], Bp, Bq);
+              constexpr int m2 = -mp - l;            // term with I_j^{-mp}
+              if constexpr (mp > 0 && m2 >= -n) {
+                constexpr int ma = -m2;
+                constexpr float s = (ma & 1) ? -1.f : 1.f;
+                if constexpr (ps == 2) L[o] = __ffma2_rn(make_float2(s * Mr[ci(n, ma)], s * Mr[ci(n, ma)]), Cp, L[o]);
+                else L[o] = __ffma2_rn(make_float2(-s * Mi[ci(n, ma)], -s * Mi[ci(n, ma)]), Cq, L[o]);
+              }
             }
-          }
-          constexpr int m2 = -mp - l;              // term with I_j^{-mp}
-          if constexpr (mp > 0 && m2 >= -n) {
-            constexpr float s = ((-m2) & 1) ? -1.f : 1.f;
-            cmac2(L[o], s * Mr[ci(n, -m2)], -s * Mi[ci(n, -m2)], Cp, Cq);
-          }
+          });
         });
       });
     });

@@ -24,10 +24,11 @@
 // has such a close pair); |g - g_exact| <= 2e-7 (FP32 evaluation, checked by
 // the parity tests through fmm_eval_cutoff).  The pair arithmetic of the two
 // targets of a lane is packed into FP32x2 (FFMA2) with the source operands
-// broadcast, halving the issue slots per pair.  Source
-// tiles whose every pair has rho >= 4.5 (checked per tile from the leaf
-// boxes and the tile's largest sigma) take the exact singular branch: there
-// 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
+// broadcast, halving the issue slots per pair.  Sources whose every pair
+// with the target leaf has rho >= 4.5 (distance from the source to the leaf
+// cube >= 4.5 sqrt2 sigma_j, tested once per source while staging) are
+// compacted to the front of the tile and take the exact singular branch:
+// there 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
 #include "ctx.cuh"
 
 namespace fmmb {
@@ -108,74 +109,94 @@ __device__ __forceinline__ void zero(Acc2& A) {
 }
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// one source (q: position, -1/(2 sigma^2); a: alpha/(4 pi), 1/(sqrt2 sigma)) on
-// the lane's two targets, all arithmetic packed FP32x2 (FFMA2/FMUL2/FADD2).
-// NEAR selects the regularised kernel, else the exact singular one.
+// one source on the lane's two targets, all arithmetic packed FP32x2
+// (FFMA2/FMUL2/FADD2).  Shared-memory operands per source:
+//   q = (x', y', z', -log2(e)/(2 sigma^2))      a = (alpha/(4 pi), 1/(sqrt2 sigma))
+//   c = (1/(2 sqrt2 sigma), (2/sqrt pi)/(sqrt2 sigma), -(4/(3 sqrt pi))/(sqrt2 sigma)^3, 1/(2 sigma^2))  [NEAR only]
+// The stretching accumulators carry fp/(-3) (fp = f'/r); flush multiplies by -3.
+// NEAR selects the regularised kernel, else the exact singular one:
+//   far : f = 1/r^3,  fp/(-3) = 1/r^5
+//   near: f = g/r^3,  fp/(-3) = g/r^5 - (4/(3 sqrt pi)) (1/(sqrt2 sigma))^3 e^{-rho^2}/r^2
+//         (= ((4/sqrt pi) rho^3 e^{-rho^2} - 3 g)/r^5 / (-3)),
+//   g from erfcx with rho = r/(sqrt2 sigma) entering only through FFMA2s on r.
 template <bool NEAR>
 __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, float2 b0, float2 b1, float2 b2,
-                                      const float4 q, const float4 a) {
+                                      const float4 q, const float4 a, const float4 c) {
   const float2 rx = __fadd2_rn(x0, bc(-q.x)), ry = __fadd2_rn(x1, bc(-q.y)), rz = __fadd2_rn(x2, bc(-q.z));
   const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
   const float2 inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
   const float2 inv2 = __fmul2_rn(inv, inv);
   const float2 inv3 = __fmul2_rn(inv2, inv);
-  float2 f, fp;
+  float2 f, fp3;
   if (NEAR) {
-    const float2 x = __fmul2_rn(r2, bc(-q.w));                 // rho^2
-    const float2 ea = __fmul2_rn(x, bc(-1.4426950408889634f));
+    const float2 ea = __fmul2_rn(r2, bc(q.w));                 // -rho^2 log2(e)
     const float2 e = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
-    const float2 rho = __fmul2_rn(__fmul2_rn(r2, inv), bc(a.w));
-    const float2 g = erfcx_g(rho, e);
+    const float2 r = __fmul2_rn(r2, inv);
+    // g = 1 - e (h(t) + (2/sqrt pi) rho), h ~ erfcx, t = 1/(1 + rho/2)
+    const float2 d = __ffma2_rn(r, bc(c.x), bc(1.f));
+    const float2 tt = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+    float2 h = bc(6.501056254e-02f);
+    const float hc[6] = {-4.661040902e-01f, 9.906343818e-01f, -3.476467133e-01f, 5.238698721e-01f,
+                         2.293880880e-01f, 4.825282376e-03f};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) h = __ffma2_rn(h, tt, bc(hc[k]));
+    const float2 y = __ffma2_rn(r, bc(c.y), h);
+    const float2 g = __ffma2_rn(make_float2(-e.x, -e.y), y, bc(1.f));
     f = __fmul2_rn(g, inv3);
-    const float2 t1 = __fmul2_rn(__fmul2_rn(rho, x), bc(2.2567583341910252f));   // (4/sqrt pi) rho^3
-    fp = __fmul2_rn(__ffma2_rn(t1, e, __fmul2_rn(g, bc(-3.0f))), __fmul2_rn(inv3, inv2));
+    fp3 = __ffma2_rn(bc(c.z), __fmul2_rn(e, inv2), __fmul2_rn(f, inv2));
     // close pairs (rho < 0.8, evaluated only when some lane of the warp has
     // one): f = g/r^3 and f'/r from the Taylor series in x = rho^2 without
     // dividing by r, so they stay exact as r -> 0 (r = 0 still contributes 0, Z7):
     //   f = k^{3/2} s(x),  f'/r = k^{5/2} T(x),  k = 1/(2 sigma^2)
-    if (__any_sync(0xffffffffu, fminf(x.x, x.y) < 0.64f)) {
+    constexpr float ea_close = -0.64f * 1.4426950408889634f;
+    if (__any_sync(0xffffffffu, fmaxf(ea.x, ea.y) > ea_close)) {
+      const float kk = c.w, k32 = kk * a.w, k52 = kk * k32;
+      const float2 x = __fmul2_rn(r2, bc(kk));
       const float2 sx = series_s(x), tx = series_t(x);
-      const float kk = -q.w, k32 = kk * a.w, k52 = kk * k32;
-      f = make_float2(x.x < 0.64f ? (r2.x > 0.f ? k32 * sx.x : 0.f) : f.x,
-                      x.y < 0.64f ? (r2.y > 0.f ? k32 * sx.y : 0.f) : f.y);
-      fp = make_float2(x.x < 0.64f ? (r2.x > 0.f ? k52 * tx.x : 0.f) : fp.x,
-                       x.y < 0.64f ? (r2.y > 0.f ? k52 * tx.y : 0.f) : fp.y);
+      const bool c0 = ea.x > ea_close, c1 = ea.y > ea_close;
+      f = make_float2(c0 ? (r2.x > 0.f ? k32 * sx.x : 0.f) : f.x, c1 ? (r2.y > 0.f ? k32 * sx.y : 0.f) : f.y);
+      fp3 = make_float2(c0 ? (r2.x > 0.f ? (-1.f / 3.f) * k52 * tx.x : 0.f) : fp3.x,
+                        c1 ? (r2.y > 0.f ? (-1.f / 3.f) * k52 * tx.y : 0.f) : fp3.y);
     }
   } else {
     f = inv3;
-    fp = __fmul2_rn(__fmul2_rn(inv3, inv2), bc(-3.0f));
+    fp3 = __fmul2_rn(inv3, inv2);
   }
   const float2 c0 = __ffma2_rn(bc(a.y), rz, __fmul2_rn(bc(-a.z), ry));
   const float2 c1 = __ffma2_rn(bc(a.z), rx, __fmul2_rn(bc(-a.x), rz));
   const float2 c2 = __ffma2_rn(bc(a.x), ry, __fmul2_rn(bc(-a.y), rx));
   A.u0 = __ffma2_rn(f, c0, A.u0); A.u1 = __ffma2_rn(f, c1, A.u1); A.u2 = __ffma2_rn(f, c2, A.u2);
   A.a0 = __ffma2_rn(f, bc(a.x), A.a0); A.a1 = __ffma2_rn(f, bc(a.y), A.a1); A.a2 = __ffma2_rn(f, bc(a.z), A.a2);
-  const float2 qq = __fmul2_rn(fp, __ffma2_rn(rz, b2, __ffma2_rn(ry, b1, __fmul2_rn(rx, b0))));
+  const float2 qq = __fmul2_rn(fp3, __ffma2_rn(rz, b2, __ffma2_rn(ry, b1, __fmul2_rn(rx, b0))));
   A.s0 = __ffma2_rn(qq, c0, A.s0); A.s1 = __ffma2_rn(qq, c1, A.s1); A.s2 = __ffma2_rn(qq, c2, A.s2);
 }
 
-struct DAcc {
-  double u0, u1, u2, s0, s1, s2, a0, a1, a2;
-};
-
-__device__ __forceinline__ void flush(DAcc& D0, DAcc& D1, const Acc2& A) {
-  D0.u0 += A.u0.x; D0.u1 += A.u1.x; D0.u2 += A.u2.x;
-  D0.s0 += A.s0.x; D0.s1 += A.s1.x; D0.s2 += A.s2.x;
-  D0.a0 += A.a0.x; D0.a1 += A.a1.x; D0.a2 += A.a2.x;
-  D1.u0 += A.u0.y; D1.u1 += A.u1.y; D1.u2 += A.u2.y;
-  D1.s0 += A.s0.y; D1.s1 += A.s1.y; D1.s2 += A.s2.y;
-  D1.a0 += A.a0.y; D1.a1 += A.a1.y; D1.a2 += A.a2.y;
+// per-target FP64 accumulators live in shared memory ([quantity][lane], 18
+// per lane: the two targets' u, s, sum f alpha), freeing 36 registers for
+// occupancy; each FP32 tile partial is added once per tile.
+constexpr int kDQ = 18;
+__device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A) {
+  const float2 v[9] = {A.u0, A.u1, A.u2, A.s0, A.s1, A.s2, A.a0, A.a1, A.a2};
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const double w = q >= 3 && q < 6 ? -3.0 : 1.0;     // s carries fp/(-3)
+    sD[q][lane] += w * (double)v[q].x;
+    sD[9 + q][lane] += w * (double)v[q].y;
+  }
 }
 
-__global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
+template <int MINB, int UF, int UN>
+__global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             double px, double py, double pz,
                                             const float4* __restrict__ pos, const float4* __restrict__ alp,
                                             float* __restrict__ un, float* __restrict__ sn,
                                             unsigned long long* __restrict__ near_pairs) {
-  __shared__ float4 sx[TP];   // (x', y', z', -1/(2 sigma^2))
+  __shared__ float4 sx[TP];   // (x', y', z', -log2(e)/(2 sigma^2))
   __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
+  __shared__ float4 sc[TP];   // near-kernel constants of the source (see pair2)
+  __shared__ double sD[kDQ][NT];
   const float k4 = (float)(1.0 / (4.0 * kPi));
   const int lane = threadIdx.x;
   const int leaf = leaf_ids[blockIdx.x];
@@ -202,7 +223,8 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
       x10 = (float)((double)p.x - cx); x11 = (float)((double)p.y - cy); x12 = (float)((double)p.z - cz);
       a1 = alp[tb + i1];
     }
-    DAcc D0 = {0, 0, 0, 0, 0, 0, 0, 0, 0}, D1 = D0;
+#pragma unroll
+    for (int q = 0; q < kDQ; ++q) sD[q][lane] = 0.0;
     for (int e = eb; e < ee; ++e) {
       const uint64_t ent = lst[e];
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
@@ -214,7 +236,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
         // stage the tile, far sources first: a source is "far" when it is
         // >= 4.5 sqrt2 sigma_j from the whole target leaf cube, so every pair
         // it forms has rho >= 4.5 (then 1 - g < 1e-8: the exact singular branch)
-        float4 qv[2], av[2];
+        float4 qv[2], av[2], cv[2];
         bool fj[2], vj[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -226,8 +248,10 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
             const float4 a = alp[sb + j];
             const float w = 1.0f / (2.0f * p.w * p.w);
             const float qx = (float)((double)p.x + shx), qy = (float)((double)p.y + shy), qz = (float)((double)p.z + shz);
-            qv[h] = make_float4(qx, qy, qz, -w);
-            av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, sqrtf(w));
+            const float aw = sqrtf(w);
+            qv[h] = make_float4(qx, qy, qz, -1.4426950408889634f * w);
+            av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
+            cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx) - hst), gy = fmaxf(0.f, fabsf(qy) - hst), gz = fmaxf(0.f, fabsf(qz) - hst);
             fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
           }
@@ -244,6 +268,7 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
                                 : nfar + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
           sx[dst] = qv[h];
           sa[dst] = av[h];
+          sc[dst] = cv[h];
         }
         __syncwarp();
         nnear += (unsigned long long)(nj - nfar) * (unsigned long long)min(TP, tcnt - t0);
@@ -251,27 +276,26 @@ __global__ void __launch_bounds__(NT, 16) k_p2p(const int* __restrict__ leaf_ids
         zero(A);
         const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
         const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
-#pragma unroll 4
-        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
-#pragma unroll 2
-        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj]);
-        flush(D0, D1, A);
+#pragma unroll UF
+        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sa[jj]);
+#pragma unroll UN
+        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sc[jj]);
+        flush(sD, lane, A);
       }
     }
     // s += (sum_j f alpha_j) x alpha_i
-    if (v0) {
-      const int64_t o = 3 * (int64_t)(tb + i0);
-      un[o] = (float)D0.u0; un[o + 1] = (float)D0.u1; un[o + 2] = (float)D0.u2;
-      sn[o] = (float)(D0.s0 + (D0.a1 * a0.z - D0.a2 * a0.y));
-      sn[o + 1] = (float)(D0.s1 + (D0.a2 * a0.x - D0.a0 * a0.z));
-      sn[o + 2] = (float)(D0.s2 + (D0.a0 * a0.y - D0.a1 * a0.x));
-    }
-    if (v1) {
-      const int64_t o = 3 * (int64_t)(tb + i1);
-      un[o] = (float)D1.u0; un[o + 1] = (float)D1.u1; un[o + 2] = (float)D1.u2;
-      sn[o] = (float)(D1.s0 + (D1.a1 * a1.z - D1.a2 * a1.y));
-      sn[o + 1] = (float)(D1.s1 + (D1.a2 * a1.x - D1.a0 * a1.z));
-      sn[o + 2] = (float)(D1.s2 + (D1.a0 * a1.y - D1.a1 * a1.x));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!(h == 0 ? v0 : v1)) continue;
+      const float4 ai = h == 0 ? a0 : a1;
+      const double* D = &sD[9 * h][lane];
+      const double u0 = D[0 * NT], u1 = D[1 * NT], u2 = D[2 * NT], s0 = D[3 * NT], s1 = D[4 * NT], s2 = D[5 * NT];
+      const double f0 = D[6 * NT], f1 = D[7 * NT], f2 = D[8 * NT];
+      const int64_t o = 3 * (int64_t)(tb + (h == 0 ? i0 : i1));
+      un[o] = (float)u0; un[o + 1] = (float)u1; un[o + 2] = (float)u2;
+      sn[o] = (float)(s0 + (f1 * ai.z - f2 * ai.y));
+      sn[o + 1] = (float)(s1 + (f2 * ai.x - f0 * ai.z));
+      sn[o + 2] = (float)(s2 + (f0 * ai.y - f1 * ai.x));
     }
   }
   if (lane == 0 && nnear) atomicAdd(near_pairs, nnear);
@@ -292,8 +316,11 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   c.dnear.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
-  FMM_LAUNCH(c, k_p2p, (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc, c.lo[0], c.lo[1],
-             c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.pos.p, c.alp.p, u_near, s_near, c.dnear.p);
+  // 16 blocks/SM (128 registers), far loop unrolled 4x, near 2x: the best of
+  // the occupancy/unroll sweep on C3 (tools/p2p_sweep.py history)
+  FMM_LAUNCH(c, (k_p2p<16, 4, 2>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
+             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.pos.p, c.alp.p, u_near, s_near,
+             c.dnear.p);
 }
 
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {

@@ -7,7 +7,7 @@ the two source loops of k_p2p (backward branches), counts FADD2 + FMUL2 +
 2 FFMA2 per loop body (+ scalar FADD/FMUL/FFMA), excludes forward-branched
 blocks inside the body (the close-pair series, only taken when some lane has
 rho < 0.8), and divides by the pairs the body evaluates (two LDS.128 per
-source, two targets per lane).  Returns {"near": F_near, "far": F_far}.
+source, three for the near kernel; two targets per lane).  Returns {"near": F_near, "far": F_far}.
 """
 from __future__ import annotations
 
@@ -72,13 +72,13 @@ def p2p_flops_per_pair(lib):
                 continue
             o = _op(t)[0].split(".")[0]
             cnt[o] = cnt.get(o, 0) + 1
-        sources = cnt.get("LDS", 0) // 2
+        kind = "near" if "MUFU" in "".join(t for _, t in body) and any("EX2" in t for _, t in body) else "far"
+        sources = cnt.get("LDS", 0) // (3 if kind == "near" else 2)   # q, a (+ c for the near kernel)
         if sources == 0:
             continue
         packed = cnt.get("FADD2", 0) + cnt.get("FMUL2", 0) + 2 * cnt.get("FFMA2", 0)
         scalar = cnt.get("FADD", 0) + cnt.get("FMUL", 0) + 2 * cnt.get("FFMA", 0)
         per_pair = (2 * packed + scalar) / (2.0 * sources)
-        kind = "near" if "MUFU" in "".join(t for _, t in body) and any("EX2" in t for _, t in body) else "far"
         res[kind] = max(res.get(kind, 0.0), per_pair)
     return res
 
