@@ -81,6 +81,9 @@ typedef struct {
                                     axis (reading Z27, weak scaling); tiles[d] in {1, 2},
                                     default (1,1,1).  With tiles != (1,1,1) rank r owns
                                     tile/top octant r and nranks = tiles product       */
+  int32_t  m2l_path;             /* 0 (default): tensor-core M2L (tcgen05, 3xTF32) on the
+                                    levels whose cells share one offset set, register
+                                    kernel elsewhere; 1: register (CUDA-core) kernel only */
 } fmm_config;
 
 /* Per-phase device times of the last set_particles / evaluate (CUDA events on
@@ -104,6 +107,7 @@ typedef struct {
   int64_t  let_bytes_sent, let_bytes_recv;  /* reply payload bytes                       */
   int64_t  let_cells, let_leaves;           /* remote multipoles / leaves received         */
   double   ms_let;                          /* exchange time (CUDA events, incl. requests) */
+  int64_t  m2l_tc_list;                     /* M2L entries evaluated on the tensor cores    */
 } fmm_stats;
 
 /* Fill cfg with the defaults listed above. */

@@ -186,6 +186,7 @@ FMM_API void fmm_config_default(fmm_config* cfg) {
   cfg->nranks = 1;
   cfg->nccl_id = nullptr;
   cfg->tiles[0] = cfg->tiles[1] = cfg->tiles[2] = 1;
+  cfg->m2l_path = 0;
 }
 
 FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
@@ -299,6 +300,7 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->nlevels = c.level_begin.empty() ? 0 : (int64_t)c.level_begin.size() - 1;
   s->p2p_list = c.np2p;
   s->m2l_list = c.nm2l;
+  s->m2l_tc_list = c.tc_entries;
   s->p2p_pairs = c.p2p_pairs;
   s->far_m2l = c.far_m2l;
   s->model_flops = 174.0 * (double)c.p2p_pairs;

@@ -19,6 +19,12 @@ struct Cells {
   }
 };
 
+// a level whose cells all take the tensor-core M2L (m2l_tc.cu)
+struct TcLevel {
+  int lt = 0, D = 0, ntgt = 0;
+  int64_t tgt_off = 0, code_off = 0, op_off = 0;
+};
+
 enum Phase { PH_SET0, PH_KEYS, PH_SORT, PH_TREE, PH_EVAL0, PH_UP, PH_TRAV, PH_M2L, PH_P2P, PH_DOWN, PH_FIN, PH_N };
 
 struct Ctx {
@@ -70,6 +76,14 @@ struct Ctx {
   DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;
   DBuf<unsigned long long> dcount, dnear;
   int64_t p2p_near_pairs = 0;                // pairs of the last P2P on regularised tiles
+  // tensor-core M2L (m2l_tc.cu): decided once per list build
+  bool tc_valid = false;
+  std::vector<TcLevel> tc_levels;
+  int64_t tc_entries = 0;                    // M2L list entries handled by the tensor path
+  DBuf<unsigned char> tc_skip;               // [ncells] 1 = the register kernel skips the cell
+  DBuf<int> tc_tmp, tc_codes_tmp, tc_tgt, tc_codes, tc_cnt;
+  DBuf<short> tc_tbl;
+  DBuf<unsigned char> tc_op;                 // pre-split operators, [level][d][K-block][hi|lo]
 
   // ---- expansions and results ----
   DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)
@@ -97,6 +111,8 @@ void build_lists(Ctx& c);
 void upward_pass(Ctx& c);
 void m2l_pass(Ctx& c);
 bool m2l_pass_reg(Ctx& c);
+void m2l_tc_prepare(Ctx& c);
+void m2l_tc_run(Ctx& c);
 bool l2p_pass_reg(Ctx& c, float* u_far, float* s_far);
 void comm_init(Ctx& c);
 void comm_unique_id(void* out);

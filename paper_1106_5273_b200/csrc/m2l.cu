@@ -132,14 +132,15 @@ __device__ void irregular_column_x(float x, float y, float z, int m, float4* __r
 template <int P>
 __global__ void __launch_bounds__(32) k_m2l_reg(const int* __restrict__ seg_b, const int* __restrict__ seg_e,
                                                 const uint64_t* __restrict__ lst, MCells c,
-                                                const float2* __restrict__ M, float2* __restrict__ Lc) {
+                                                const float2* __restrict__ M, float2* __restrict__ Lc,
+                                                const unsigned char* __restrict__ skip) {
   using D = Dims<P>;
   constexpr int NC = D::NC, P2 = D::P2, S = D::S;
   extern __shared__ float4 sm4[];                  // [kSub][S] harmonics, later the reduction buffer
   __shared__ float4 Dsh[kSub];
   const int t = blockIdx.x;
   const int b = seg_b[t], e = seg_e[t];
-  if (b == e) return;
+  if (b == e || skip[t]) return;                   // empty, or taken by the tensor-core path
   const int lane = threadIdx.x;
   const int sub = lane / 3, comp = lane - 3 * (lane / 3);
   const bool act = sub < kSub;
@@ -239,7 +240,8 @@ void launch_reg(Ctx& c) {
   size_t red = sizeof(float2) * (size_t)kSub * 3 * D::NC;
   if (red > sm) sm = red;
   MCells mc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, {c.per_units[0], c.per_units[1], c.per_units[2]}};
-  FMM_LAUNCH(c, k_m2l_reg<P>, (unsigned)c.ncells, 32, sm, c.m2l_b.p, c.m2l_e.p, c.m2l.p, mc, c.M.p, c.Lc.p);
+  FMM_LAUNCH(c, k_m2l_reg<P>, (unsigned)c.ncells, 32, sm, c.m2l_b.p, c.m2l_e.p, c.m2l.p, mc, c.M.p, c.Lc.p,
+             c.tc_skip.p);
 }
 
 }  // namespace

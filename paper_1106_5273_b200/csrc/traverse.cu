@@ -140,6 +140,7 @@ void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
 }  // namespace
 
 void build_lists(Ctx& c) {
+  c.tc_valid = false;
   cudaStream_t st = c.stream;
   c.np2p = c.nm2l = 0;
   c.p2p_pairs = 0;

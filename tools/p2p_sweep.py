@@ -18,12 +18,13 @@ def main():
     ap.add_argument("--variants", default="0")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--full", action="store_true", help="also time full evaluate phases")
+    ap.add_argument("--m2l-path", type=int, default=0)
     args = ap.parse_args()
     import torch
     import paper_1106_5273_b200 as P
     import synth
     x, a, s = synth.taylor_green(args.side)
-    f = P.FMM(order=10, images=3, theta=(1, 2), ncrit=64)
+    f = P.FMM(order=10, images=3, theta=(1, 2), ncrit=64, m2l_path=args.m2l_path)
     xt, at, st = (torch.from_numpy(v).cuda() for v in (x, a, s))
     f.set_particles(xt, at, st)
     n = len(x)
@@ -52,6 +53,7 @@ def main():
         torch.cuda.synchronize()
         st = f.stats()
         print({k: round(v, 2) for k, v in st.items() if k.startswith("ms_")})
+        print("m2l_list %d  m2l_tc_list %d" % (st["m2l_list"], st["m2l_tc_list"]))
     f.close()
 
 
