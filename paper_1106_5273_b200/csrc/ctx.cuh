@@ -81,7 +81,8 @@ struct Ctx {
   std::vector<TcLevel> tc_levels;
   int64_t tc_entries = 0;                    // M2L list entries handled by the tensor path
   DBuf<unsigned char> tc_skip;               // [ncells] 1 = the register kernel skips the cell
-  DBuf<int> tc_tmp, tc_codes_tmp, tc_tgt, tc_codes, tc_cnt;
+  DBuf<int> tc_tmp, tc_codes_tmp, tc_tgt, tc_tgt2, tc_codes, tc_cnt;
+  DBuf<float> tc_mp;                         // packed multipoles [cell][3][112] for the row gathers
   DBuf<short> tc_tbl;
   DBuf<unsigned char> tc_op;                 // pre-split operators, [level][d][K-block][hi|lo]
 

@@ -2,44 +2,59 @@
 // the levels where every target cell sees the same set of source offsets.
 //
 // In a uniform periodic octree every cell of a level has the same M2L
-// interaction list up to translation: the same D offsets (source level and
-// centre offset Delta), in some traversal order.  For a fixed offset d the
-// M2L translation is a fixed real-linear map T_d from the source multipole
+// interaction list up to translation and up to the mirror symmetry of its
+// octant in the parent: a cell of parity class c = (qx&1, qy&1, qz&1) sees
+// the offsets Q_c(S), S the set of the even (class 0) cells and Q_c the
+// reflection of the axes whose bit is set.  For a fixed offset d the M2L
+// translation is a fixed real-linear map T_d from the source multipole
 // (p(p+1)/2 complex = 110 reals at p = 10, component-wise) to the target local
-// expansion, so for a level the whole M2L is one dense contraction
+// expansion, and a reflection only changes signs:
 //
-//   L[(t, c), j] += sum_d sum_i  M[(src(t, d), c), i]  T_d[j, i]
+//   T(Q D) = S_L(Q) T(D) S_M(Q),   S diagonal +-1:
+//     x: (n,m) -> (-1)^m conj,  y: conj,  z: (-1)^(n+m)      (I_n^m(QD) likewise)
 //
-// with K = D x 112 (110 padded): the shape tcgen05.mma wants.  Rows are
-// (target cell, vorticity component), 512 per CTA as four 128-row
-// accumulators (4 x 112 of the 512 TMEM columns); the operator T_d is built
-// once per level in double precision from I_{n+k}^{m+l}(D) with the
-// (-1)^k sign and the (s_s/s_t)^n scale of P:228 folded in.
+// so a whole level is ONE dense contraction with one operator,
+//
+//   L[(t, c), j] += S_L(t)_j sum_d sum_i T_d[j, i] S_M(t)_i M[(src(t, d), c), i],
+//
+// K = D x 112 (110 padded): the shape tcgen05.mma wants.  T_d is built once per
+// level in double precision from I_{n+k}^{m+l}(D) with the (-1)^k sign and the
+// (s_s/s_t)^n scale of P:228 folded in.  The triangular truncation n + k <= p-1
+// makes the rows of T_d that a K-block of inputs (degrees >= n_min) reaches a
+// prefix of length (p - n_min)(p - n_min + 1): each K-block's MMA uses only that
+// many output columns (N = 112, 80, 64, 48, 32, 32, 32, 16 x 7 at p = 10, a third
+// of the dense work) and the operator stores only those rows.
 //
 // Precision (3xTF32): every operand is split x = hi + lo, hi = x with the 13
 // low mantissa bits cleared (exactly a TF32 value), lo = x - hi; the product
-// is accumulated as hi.hi + lo.hi + hi.lo in FP32 in TMEM (relative error
-// ~2^-21, FP32-level; 1xTF32 would be ~1e-3, tools/umma_probe.cu).
+// is accumulated as hi.hi + lo.hi + hi.lo in FP32 in TMEM.  The tensor cores
+// accumulate with truncation (tools/umma_probe.cu: the error grows ~1e-8 per
+// MMA), so the accumulators are drained into Lc every kChunk offsets; the
+// result then matches the FP32 register kernel's accuracy against the
+// oracle (tests/test_gpu_m2l_tc.py).
 //
-// Pipeline (one CTA per SM, 17 warps): warps 0-15 own one row each -- they
-// gather the row's 8 multipole reals of the current K-block from global
-// memory (prefetched two stages ahead), split them and store hi/lo into the
-// stage's A tiles (K-major core-matrix layout, no swizzle); thread 0 also
-// starts the bulk copy (cp.async.bulk + mbarrier tx count) of the stage's
-// pre-split operator slice.  Warp 16 allocates TMEM and one thread issues the
-// 12 MMAs of a stage (4 accumulators x 3 products), committing to the stage's
-// "empty" mbarrier.  Every kChunk offsets the producers drain the
-// accumulators (TMEM lane quarter = warp % 4) into Lc and the MMAs restart.
+// Pipeline (two CTAs per SM, 9 warps each): rows are (target, component),
+// 256 per CTA as two 128-row accumulators in TMEM.  Warps 0-7 gather the 8
+// multipole reals of the current K-block for every row from a 16-byte-aligned
+// packed copy of M (two threads per row, one 16-byte chunk each), apply the
+// row's S_M signs, split hi/lo and store the stage's A tiles (K-major
+// core-matrix layout, no swizzle); thread 0 also bulk-copies the stage's
+// pre-split operator slice (cp.async.bulk, mbarrier tx count).  One thread of
+// warp 8 issues the 6 MMAs of a stage and commits to the stage's "empty"
+// mbarrier.  Targets are processed in Morton order so concurrently running
+// CTAs share their sources in L2.
 //
-// Which cells take this path is decided per list build: a reference cell's
-// offsets define the level's canonical set; a verification kernel checks,
-// for every cell of the level, that its list has exactly those offsets and
-// that the source the tensor kernel will compute (Morton index of the
-// offset cell in the level-ordered cell array) is the list's source.  Cells
-// that fail (adaptive trees, partial levels, other ranks' cells) stay on the
-// register kernel (m2l.cu), which skips the cells taken here.
+// Which cells take this path is decided per list build: a reference cell
+// fixes the level's canonical offsets; a verification kernel checks for every
+// cell that its list, reflected into class 0, is exactly that set and that the
+// source the tensor kernel computes (Morton index of the offset cell in the
+// level-ordered cell array) is the list's source.  Cells that fail (adaptive
+// trees, partial levels) stay on the register kernel (m2l.cu), which skips
+// the cells taken here.
 #include <algorithm>
 #include <cstring>
+
+#include <cub/cub.cuh>
 
 #include "ctx.cuh"
 
@@ -47,19 +62,28 @@ namespace fmmb {
 
 namespace {
 
-constexpr int kRows = 512;                  // rows (target, component) per CTA
-constexpr int kN = 112;                     // local-expansion reals (110 at p = 10, padded)
+#ifndef TC_CHUNK
+#define TC_CHUNK 16
+#endif
+#ifndef TC_PF
+#define TC_PF 4
+#endif
+constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
+constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
+constexpr int kRows = 256;                  // rows (target, component) per CTA
+constexpr int kN = 112;                     // local-expansion reals (110, padded)
 constexpr int kKB = 8;                      // K per stage (one kind::tf32 MMA)
 constexpr int kNKB = 14;                    // K-blocks per offset (112 / 8)
 constexpr int kStages = 4;
+constexpr int kPF = TC_PF;                      // gather prefetch distance (stages)
 constexpr int kATile = 128 * kKB * 4;       // one 128-row A tile (hi or lo), bytes
-constexpr int kAStage = 4 * 2 * kATile;     // 4 accumulators x (hi, lo)
-constexpr int kBHalf = kN * kKB * 4;        // operator slice (hi or lo), bytes
-constexpr int kStage = kAStage + 2 * kBHalf;
+constexpr int kAStage = 2 * 2 * kATile;     // 2 accumulators x (hi, lo)
+constexpr int kBMax = 2 * kN * kKB * 4;     // operator slice (hi + lo) at N = 112
+constexpr int kStage = kAStage + kBMax;
 constexpr int kThreads = kRows + 32;
-constexpr int kChunk = 16;                  // offsets accumulated in TMEM between drains
-constexpr int kMaxTcLevels = 32;   // (level, parity class) groups
-constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
+constexpr int kChunk = TC_CHUNK;                  // offsets accumulated in TMEM between drains
+constexpr int kMaxTcLevels = 16;
+constexpr int kMp = 112;                    // packed multipole stride (floats)
 
 // ---------------------------------------------------------------- PTX ----
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -90,7 +114,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 // K-major, no-swizzle operand: core matrices of 8 rows x 16 B; LBO = next
-// 16-byte K chunk, SBO = next 8 rows (128 B).
+// 16-byte K chunk, SBO = next 8 rows (128 B); descriptor version 1 (sm_100).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo) {
   return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) | (1ull << 46);
 }
@@ -104,7 +128,18 @@ __device__ __forceinline__ void umma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
                : "memory");
 }
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__host__ __device__ __forceinline__ float tf32_hi(float x) {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+#else
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u &= 0xffffe000u;
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
+#endif
+}
 
 // ------------------------------------------------------------ geometry ----
 struct TcGeo {
@@ -125,18 +160,29 @@ __device__ __forceinline__ uint32_t spread3_32(uint32_t v) {   // 10-bit spread 
 // offset code: (dl + 1) << 21 | (vx + 64) << 14 | (vy + 64) << 7 | (vz + 64),
 // dl = level_s - level_t in {-1, 0, 1}, v = Delta / 2^(21 - max(lt, ls)) with
 // Delta = c_t - c_s - image shift in half-finest-cell units.
-__device__ __forceinline__ int code_dl(int code) { return (code >> 21) - 1; }
-__device__ __forceinline__ int code_v(int code, int a) { return ((code >> (14 - 7 * a)) & 127) - 64; }
+__host__ __device__ __forceinline__ int code_dl(int code) { return (code >> 21) - 1; }
+__host__ __device__ __forceinline__ int code_v(int code, int a) { return ((code >> (14 - 7 * a)) & 127) - 64; }
+// Q_c: negate the offset components of the axes whose class bit is set
+__host__ __device__ __forceinline__ int reflect(int code, int cls) {
+  int out = code & (3 << 21);
+  for (int a = 0; a < 3; ++a) {
+    const int v = code_v(code, a);
+    out |= ((((cls >> a) & 1) ? -v : v) + 64) << (14 - 7 * a);
+  }
+  return out;
+}
 
-// the cell the tensor kernel reads for target t (centre ct) and offset code:
+// the cell the tensor kernel reads for a target (centre ct) and offset code:
 // c_s = c_t - Delta wrapped into the period, its level-ls Morton index
-__device__ __forceinline__ int tc_source(const TcGeo& g, int lt, const long long (&ct)[3], int code) {
+// (centres and periods are < 2^23 half-finest-cell units: int arithmetic)
+template <typename I>
+__device__ __forceinline__ int tc_source(const TcGeo& g, int lt, const I (&ct)[3], int code) {
   const int dl = code_dl(code), ls = lt + dl, lf = max(lt, ls);
   uint32_t q[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    long long cs = ct[a] - (long long)code_v(code, a) * (1ll << (kMaxLevel - lf));
-    const long long P = g.per[a];
+    const int P = (int)g.per[a];
+    int cs = (int)ct[a] - code_v(code, a) * (1 << (kMaxLevel - lf));
     cs %= P;
     if (cs < 0) cs += P;
     q[a] = (uint32_t)(((cs >> (kMaxLevel - ls)) - 1) >> 1);
@@ -172,6 +218,66 @@ __device__ __forceinline__ void centre(const TcGeo& g, int cell, int lt, long lo
   ct[2] = (long long)(2 * g.qz[cell] + 1) << (kMaxLevel - lt);
 }
 
+// parity class of a cell: its octant within the parent
+__device__ __forceinline__ int parity_class(const TcGeo& g, int c) {
+  return (g.qx[c] & 1) | ((g.qy[c] & 1) << 1) | ((g.qz[c] & 1) << 2);
+}
+
+// (degree, order) of complex coefficient o = n(n+1)/2 + m
+__host__ __device__ __forceinline__ void deg_ord(int o, int& n, int& m) {
+  n = 0;
+  while ((n + 1) * (n + 2) / 2 <= o) ++n;
+  m = o - n * (n + 1) / 2;
+}
+// sign of real r = 2 o + part of a coefficient under the class-c reflection
+// (the same pattern for multipoles and locals, see the header)
+inline bool refl_negates(int r, int cls) {
+  if (r >= 2 * kNC) return false;
+  int n, m;
+  deg_ord(r >> 1, n, m);
+  const int im = r & 1;
+  int neg = 0;
+  if (cls & 1) neg ^= (m & 1) ^ im;
+  if (cls & 2) neg ^= im;
+  if (cls & 4) neg ^= (n + m) & 1;
+  return neg != 0;
+}
+
+// output columns the K-block kb reaches (rows of T_d that are not zero)
+inline int kb_cols(int kb) {
+  int n, m;
+  deg_ord(4 * kb, n, m);                     // lowest degree in the K-block
+  const int kmax = kTcP - 1 - n;
+  const int rows = (kmax + 1) * (kmax + 2);
+  return std::min(kN, std::max(16, (rows + 15) / 16 * 16));
+}
+
+struct TcTables {
+  int ncols[kNKB];           // N of each K-block's MMA
+  int opk[kNKB + 1];         // byte offset of each K-block's slice within one offset's operator
+  unsigned char sm[8][kNKB]; // S_M: bit q set = input real 8 kb + q negated, per class
+  uint32_t sl[8][4];         // S_L: bit j set = output real j negated, per class
+};
+
+TcTables make_tables() {
+  TcTables T{};
+  int off = 0;
+  for (int kb = 0; kb < kNKB; ++kb) {
+    T.ncols[kb] = kb_cols(kb);
+    T.opk[kb] = off;
+    off += 2 * T.ncols[kb] * kKB * 4;
+  }
+  T.opk[kNKB] = off;
+  for (int c = 0; c < 8; ++c) {
+    for (int kb = 0; kb < kNKB; ++kb)
+      for (int q = 0; q < kKB; ++q)
+        if (refl_negates(kb * kKB + q, c)) T.sm[c][kb] |= (unsigned char)(1u << q);
+    for (int j = 0; j < kN; ++j)
+      if (refl_negates(j, c)) T.sl[c][j >> 5] |= 1u << (j & 31);
+  }
+  return T;
+}
+
 // codes of one cell's entries (the level's reference cell)
 __global__ void k_tc_ref_codes(const uint64_t* __restrict__ lst, const int* __restrict__ seg_b,
                                const int* __restrict__ seg_e, int cell, int lt, TcGeo g, int* __restrict__ out) {
@@ -181,30 +287,25 @@ __global__ void k_tc_ref_codes(const uint64_t* __restrict__ lst, const int* __re
   for (int i = b + threadIdx.x; i < e; i += blockDim.x) out[i - b] = entry_code(g, lt, ct, lst[i]);
 }
 
-// parity class of a cell: its octant within the parent (the interaction
-// list of a cell depends on it, so each class has its own offset set)
-__device__ __forceinline__ int parity_class(const TcGeo& g, int c) {
-  return (g.qx[c] & 1) | ((g.qy[c] & 1) << 1) | ((g.qz[c] & 1) << 2);
-}
-
-// per class: first cell of [lb, le) with a non-empty list
-__global__ void k_tc_first(const int* __restrict__ seg_b, const int* __restrict__ seg_e, int lb, int le, TcGeo g,
+// first cell of [lb, le) with a non-empty list
+__global__ void k_tc_first(const int* __restrict__ seg_b, const int* __restrict__ seg_e, int lb, int le,
                            int* __restrict__ out) {
   for (int c = lb + blockIdx.x * blockDim.x + threadIdx.x; c < le; c += gridDim.x * blockDim.x)
-    if (seg_e[c] > seg_b[c]) atomicMin(out + parity_class(g, c), c);
+    if (seg_e[c] > seg_b[c]) atomicMin(out, c);
 }
 
-// per cell: its list is exactly the canonical offsets and every source is
-// the one tc_source computes.  Warp per cell; ok cells are appended to tgt.
+// per cell: its list, reflected into class 0, is exactly the canonical offset
+// set and every source is the one tc_source computes.  Warp per cell; ok
+// cells are appended to tgt (sorted afterwards).
 __global__ void k_tc_verify(const uint64_t* __restrict__ lst, const int* __restrict__ seg_b,
                             const int* __restrict__ seg_e, int lb, int le, int lt, int D, TcGeo g,
-                            const short* __restrict__ tbl, int R, int cls, unsigned char* __restrict__ skip,
+                            const short* __restrict__ tbl, int R, unsigned char* __restrict__ skip,
                             int* __restrict__ tgt, int* __restrict__ ntgt) {
   const int lane = threadIdx.x & 31;
   const int V = 2 * R + 1;
   for (int c = lb + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); c < le;
        c += (int)((gridDim.x * blockDim.x) >> 5)) {
-    if (parity_class(g, c) != cls) continue;
+    const int cls = parity_class(g, c);
     const int b = seg_b[c], e = seg_e[c];
     bool ok = (e - b) == D;
     long long ct[3];
@@ -214,7 +315,8 @@ __global__ void k_tc_verify(const uint64_t* __restrict__ lst, const int* __restr
       const int code = entry_code(g, lt, ct, ent);
       bool good = code >= 0;
       if (good) {
-        const int dl = code_dl(code), vx = code_v(code, 0), vy = code_v(code, 1), vz = code_v(code, 2);
+        const int c0 = reflect(code, cls);
+        const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
         good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
         if (good) good = tbl[(((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R] >= 0;
         if (good) good = tc_source(g, lt, ct, code) == (int)((ent >> 5) & 0x7ffffff);
@@ -229,14 +331,15 @@ __global__ void k_tc_verify(const uint64_t* __restrict__ lst, const int* __restr
   }
 }
 
-// operator of one level: T_d[j][i] split into TF32 hi/lo, stored per (d, K-block)
-// in the stage layout  [hi | lo] x [K chunk (2)][row group (14)][8 rows][4 floats].
-__global__ void k_tc_operator(const int* __restrict__ codes, int lt, unsigned char* __restrict__ op) {
-  constexpr int P = kTcP, NC = P * (P + 1) / 2;
+// operator of one level (class 0 offsets): T_d[j][i] split into TF32 hi/lo,
+// per (d, K-block) the rows j < ncols[kb] in the stage layout
+//   [hi | lo] x [K chunk (2)][row group (ncols / 8)][8 rows][4 floats].
+__global__ void k_tc_operator(const int* __restrict__ codes, TcTables T, unsigned char* __restrict__ op) {
+  constexpr int P = kTcP;
   const int d = blockIdx.x;
   const int code = codes[d];
   const int dl = code_dl(code);
-  __shared__ double2 I[NC];
+  __shared__ double2 I[kNC];
   __shared__ double Dv[3];
   if (threadIdx.x < 3) Dv[threadIdx.x] = (double)code_v(code, threadIdx.x) / (double)(1 << (1 + max(0, dl)));
   __syncthreads();
@@ -275,34 +378,45 @@ __global__ void k_tc_operator(const int* __restrict__ codes, int lt, unsigned ch
     return make_double2(s * v.x, -s * v.y);
   };
   const double ratio = ldexp(1.0, -dl);                 // s_s / s_t
-  unsigned char* base = op + (size_t)d * kNKB * 2 * kBHalf;
-  for (int idx = threadIdx.x; idx < kN * kN; idx += blockDim.x) {
-    const int j = idx / kN, i = idx - kN * (idx / kN);
-    double v = 0.0;
-    if (j < 2 * NC && i < 2 * NC) {
-      const int oj = j >> 1, oi = i >> 1;
-      int k = 0;
-      while ((k + 1) * (k + 2) / 2 <= oj) ++k;
-      const int l = oj - k * (k + 1) / 2;
-      int n = 0;
-      while ((n + 1) * (n + 2) / 2 <= oi) ++n;
-      const int m = oi - n * (n + 1) / 2;
-      if (n + k <= P - 1) {
-        const double2 X = Iget(n + k, m + l);
-        const double2 Y = m > 0 ? Iget(n + k, l - m) : make_double2(0.0, 0.0);
-        const double cs = (m & 1) ? -1.0 : 1.0;
-        const bool re = (j & 1) == 0, a = (i & 1) == 0;
-        // L += M X + [m > 0] (-1)^m conj(M) Y,  M = a + i b
-        if (re) v = a ? X.x + cs * Y.x : -X.y + cs * Y.y;
-        else v = a ? X.y + cs * Y.y : X.x - cs * Y.x;
-        v *= ((k & 1) ? -1.0 : 1.0) * pow(ratio, n);
+  unsigned char* base = op + (size_t)d * T.opk[kNKB];
+  for (int kb = 0; kb < kNKB; ++kb) {
+    const int nc = T.ncols[kb];
+    for (int idx = threadIdx.x; idx < nc * kKB; idx += blockDim.x) {
+      const int j = idx / kKB, kk = idx - kKB * (idx / kKB), i = kb * kKB + kk;
+      double v = 0.0;
+      if (j < 2 * kNC && i < 2 * kNC) {
+        int k, l, n, m;
+        deg_ord(j >> 1, k, l);
+        deg_ord(i >> 1, n, m);
+        if (n + k <= P - 1) {
+          const double2 X = Iget(n + k, m + l);
+          const double2 Y = m > 0 ? Iget(n + k, l - m) : make_double2(0.0, 0.0);
+          const double cs = (m & 1) ? -1.0 : 1.0;
+          const bool re = (j & 1) == 0, a = (i & 1) == 0;
+          // L += M X + [m > 0] (-1)^m conj(M) Y,  M = a + i b
+          if (re) v = a ? X.x + cs * Y.x : -X.y + cs * Y.y;
+          else v = a ? X.y + cs * Y.y : X.x - cs * Y.x;
+          v *= ((k & 1) ? -1.0 : 1.0) * pow(ratio, n);
+        }
       }
+      const float vf = (float)v, hi = tf32_hi(vf), lo = (float)(v - (double)hi);
+      const size_t off = (size_t)T.opk[kb] + (kk / 4) * (nc / 8 * 128) + (j / 8) * 128 + (j % 8) * 16 + (kk % 4) * 4;
+      *(float*)(base + off) = hi;
+      *(float*)(base + off + nc * kKB * 4) = lo;
     }
-    const float vf = (float)v, hi = tf32_hi(vf), lo = (float)(v - (double)hi);
-    const int kb = i / kKB, kk = i % kKB;
-    const size_t off = (size_t)kb * 2 * kBHalf + (kk / 4) * (kN / 8 * 128) + (j / 8) * 128 + (j % 8) * 16 + (kk % 4) * 4;
-    *(float*)(base + off) = hi;
-    *(float*)(base + off + kBHalf) = lo;
+  }
+}
+
+// packed multipoles: [cell][component][112 floats] (16-byte aligned rows, reals 110, 111 = 0)
+__global__ void k_tc_pack(const float2* __restrict__ M, int64_t ncells, float4* __restrict__ Mp) {
+  const int64_t n4 = ncells * 3 * (kMp / 4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / (kMp / 4);
+    const int q = (int)(i - row * (kMp / 4));
+    const float2* src = M + row * kNC + 2 * q;
+    const float2 a = src[0];
+    const float2 b = 2 * q + 1 < kNC ? src[1] : make_float2(0.f, 0.f);
+    Mp[i] = make_float4(a.x, a.y, b.x, b.y);
   }
 }
 
@@ -318,20 +432,21 @@ struct TcArgs {
   int nlv;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) k_m2l_tc(TcArgs args, TcGeo g, const float2* __restrict__ M,
-                                                        float2* __restrict__ Lc) {
+__global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T, TcGeo g,
+                                                        const float4* __restrict__ Mp, float2* __restrict__ Lc) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t full[kStages], empty[kStages], chunk_full, drained;
+  __shared__ uint64_t full[kStages], empty[kStages], chunk_full, drained[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
-  // this CTA's level (levels are laid out back to back, longest first)
   int li = 0;
   while (li + 1 < args.nlv && (int)blockIdx.x >= args.lv[li + 1].cta_begin) ++li;
   const TcLevelArg A = args.lv[li];
   const int nit = A.D * kNKB;
+  constexpr int CN = kChunk * kNKB;
+  const int nchunk = (nit + CN - 1) / CN;
 
   if (warp == kRows / 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(saddr(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -340,50 +455,65 @@ __global__ void __launch_bounds__(kThreads, 1) k_m2l_tc(TcArgs args, TcGeo g, co
       mbar_init(&empty[s], 1);
     }
     mbar_init(&chunk_full, 1);
-    mbar_init(&drained, kRows);
+    mbar_init(&drained[0], kRows);
+    mbar_init(&drained[1], kRows);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tbase;
+  const int row0 = ((int)blockIdx.x - A.cta_begin) * kRows;
 
   if (warp < kRows / 32) {
-    // ------------------------------------------------ producers (one row each)
-    const int row = (int)blockIdx.x - A.cta_begin;
-    const int R = row * kRows + tid;
-    const bool valid = R < 3 * A.ntgt;
-    const int t = valid ? R / 3 : 0, comp = valid ? R - 3 * (R / 3) : 0;
-    const int cell = A.tgt[t];
-    long long ct[3];
-    centre(g, cell, A.lt, ct);
-    const int tau = tid >> 7, rr = tid & 127;
-    const int arow = (rr >> 3) * 128 + (rr & 7) * 16;   // byte offset of this row's 16-byte chunk 0
+    // ---------------------------------------------------------- producers
+    // gather: rows tid/2 + 128 h (h = 0, 1), 16-byte chunk tid & 1 of each K-block
+    const int ch = tid & 1, rr = tid >> 1;
+    int ct[2][3];
+    int comp[2], cls[2];
+    const float4* src[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int R = row0 + rr + 128 * h;
+      const int t = R < 3 * A.ntgt ? R / 3 : 0;
+      comp[h] = R < 3 * A.ntgt ? R - 3 * (R / 3) : 0;
+      const int cell = A.tgt[t];
+      cls[h] = parity_class(g, cell);
+      ct[h][0] = (2 * g.qx[cell] + 1) << (kMaxLevel - A.lt);
+      ct[h][1] = (2 * g.qy[cell] + 1) << (kMaxLevel - A.lt);
+      ct[h][2] = (2 * g.qz[cell] + 1) << (kMaxLevel - A.lt);
+      src[h] = Mp;
+    }
     int pf_d = -1;
-    const float2* pf_src = M;
-    auto load = [&](int it, float2 (&v)[4]) {
+    auto load = [&](int it, float4 (&v)[2]) {
       const int d = it / kNKB, kb = it - kNKB * (it / kNKB);
       if (d != pf_d) {
         pf_d = d;
-        const int src = tc_source(g, A.lt, ct, __ldg(A.codes + d));
-        pf_src = M + ((size_t)src * 3 + comp) * 55;
+        const int code = __ldg(A.codes + d);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int s = tc_source(g, A.lt, ct[h], reflect(code, cls[h]));
+          src[h] = Mp + ((size_t)s * 3 + comp[h]) * (kMp / 4);
+        }
       }
-      const float2* p = pf_src + kb * 4;
-      v[0] = __ldg(p);
-      v[1] = __ldg(p + 1);
-      v[2] = __ldg(p + 2);
-      v[3] = kb == kNKB - 1 ? make_float2(0.f, 0.f) : __ldg(p + 3);   // reals 110, 111 are padding
+#pragma unroll
+      for (int h = 0; h < 2; ++h) v[h] = __ldg(src[h] + kb * 2 + ch);
     };
-    // drain: add the accumulator of the finished chunk into Lc.  The tensor
-    // cores accumulate FP32 with truncation, so the error grows with the
-    // number of MMAs per accumulator (tools/umma_probe.cu: ~1e-8 per MMA);
-    // draining every kChunk offsets keeps it at the FP32 register kernel's level.
-    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(tau * 128);
-    float2* out = Lc + ((size_t)cell * 3 + comp) * 55;
-    auto drain = [&](int chunk) {
+    // drains: thread tid owns row tid (TMEM lane quarter = warp % 4); the
+    // chunk's sums are added into Lc with vector reductions (REDG.ADD.F32x2:
+    // no round trip; one thread per Lc row, so the order is fixed)
+    const int Rd = row0 + tid;
+    const bool dvalid = Rd < 3 * A.ntgt;
+    const int dcell = A.tgt[dvalid ? Rd / 3 : 0], dcomp = dvalid ? Rd - 3 * (Rd / 3) : 0;
+    const int dcls = parity_class(g, dcell);
+    float2* out = Lc + ((size_t)dcell * 3 + dcomp) * kNC;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((tid >> 7) * 128);
+    int next_drain = 0;
+    auto drain = [&]() {
+      const int chunk = next_drain++;
       mbar_wait(&chunk_full, chunk & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
+#pragma unroll
       for (int c0 = 0; c0 < kN; c0 += 16) {
         uint32_t v[16];
         asm volatile(
@@ -392,86 +522,95 @@ __global__ void __launch_bounds__(kThreads, 1) k_m2l_tc(TcArgs args, TcGeo g, co
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr + c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (valid) {
+        if (dvalid) {
+          const uint32_t sg = (T.sl[dcls][c0 >> 5] >> (c0 & 31)) & 0xffffu;   // S_L of the row's class
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int o = c0 / 2 + q;
-            if (o < 55) {
-              float2 w = out[o];
-              w.x += __uint_as_float(v[2 * q]);
-              w.y += __uint_as_float(v[2 * q + 1]);
-              out[o] = w;
-            }
+            if (o < kNC)
+              atomicAdd(out + o, make_float2(__uint_as_float(v[2 * q] ^ (((sg >> (2 * q)) & 1u) << 31)),
+                                             __uint_as_float(v[2 * q + 1] ^ (((sg >> (2 * q + 1)) & 1u) << 31))));
           }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&drained);
+      mbar_arrive(&drained[chunk & 1]);
     };
-    float2 va[4], vb[4], vc[4];
-    if (nit > 0) load(0, va);
-    if (nit > 1) load(1, vb);
-    for (int it = 0; it < nit; ++it) {
-      if (it > 0 && it % (kChunk * kNKB) == 0) drain(it / (kChunk * kNKB) - 1);
-      if (it + 2 < nit) load(it + 2, vc);
-      const int s = it % kStages;
-      if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
-      unsigned char* st = smem + (size_t)s * kStage;
-      // hi / lo split, chunk c holds reals 4c..4c+3 of the K-block
-      const float x[8] = {va[0].x, va[0].y, va[1].x, va[1].y, va[2].x, va[2].y, va[3].x, va[3].y};
-      float h[8], l[8];
+    const int arow = (rr >> 3) * 128 + (rr & 7) * 16 + ch * 2048;
+    float4 buf[kPF][2];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        h[q] = tf32_hi(x[q]);
-        l[q] = x[q] - h[q];
-      }
-      unsigned char* ah = st + (tau * 2 + 0) * kATile + arow;
-      unsigned char* al = st + (tau * 2 + 1) * kATile + arow;
-      *(float4*)ah = make_float4(h[0], h[1], h[2], h[3]);
-      *(float4*)(ah + 2048) = make_float4(h[4], h[5], h[6], h[7]);
-      *(float4*)al = make_float4(l[0], l[1], l[2], l[3]);
-      *(float4*)(al + 2048) = make_float4(l[4], l[5], l[6], l[7]);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (tid == 0) {
-        const int d = it / kNKB, kb = it - kNKB * (it / kNKB);
-        mbar_arrive_tx(&full[s], 2 * kBHalf);
-        bulk_g2s(st + kAStage, A.op + ((size_t)d * kNKB + kb) * 2 * kBHalf, 2 * kBHalf, &full[s]);
-      } else {
-        mbar_arrive(&full[s]);
-      }
+    for (int u = 0; u < kPF; ++u)
+      if (u < nit) load(u, buf[u]);
+    for (int it0 = 0; it0 < nit; it0 += kPF) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { va[q] = vb[q]; vb[q] = vc[q]; }
+      for (int u = 0; u < kPF; ++u) {
+        const int it = it0 + u;
+        if (it < nit) {
+          if (it >= CN && it % CN == 0) drain();         // chunk it/CN - 1 is complete
+          const int s = it % kStages;
+          const int kb = it - kNKB * (it / kNKB);
+          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          unsigned char* st = smem + (size_t)s * kStage;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t sg = (uint32_t)(T.sm[cls[h]][kb] >> (4 * ch));    // S_M of the row's class
+            float x[4] = {buf[u][h].x, buf[u][h].y, buf[u][h].z, buf[u][h].w};
+            float hi[4], lo[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              x[q] = __uint_as_float(__float_as_uint(x[q]) ^ (((sg >> q) & 1u) << 31));
+              hi[q] = tf32_hi(x[q]);
+              lo[q] = x[q] - hi[q];
+            }
+            *(float4*)(st + (h * 2 + 0) * kATile + arow) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *(float4*)(st + (h * 2 + 1) * kATile + arow) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (tid == 0) {
+            const int d = it / kNKB;
+            const uint32_t bytes = (uint32_t)(T.opk[kb + 1] - T.opk[kb]);
+            mbar_arrive_tx(&full[s], bytes);
+            bulk_g2s(st + kAStage, A.op + (size_t)d * T.opk[kNKB] + T.opk[kb], bytes, &full[s]);
+          } else {
+            mbar_arrive(&full[s]);
+          }
+          if (it + kPF < nit) load(it + kPF, buf[u]);
+        }
+      }
     }
-    // ------------------------------------------------ epilogue: the last chunk
-    if (nit > 0) drain((nit - 1) / (kChunk * kNKB));
+    while (next_drain < nchunk) drain();
   } else if (tid == kRows) {
-    // ------------------------------------------------ MMA issuer
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    // ---------------------------------------------------------- MMA issuer
+    const uint32_t idesc0 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 4) << 24);
     for (int it = 0; it < nit; ++it) {
       const int s = it % kStages;
-      const int cit = it % (kChunk * kNKB);            // position in the chunk: 0 restarts the accumulators
-      if (it > 0 && cit == 0) mbar_wait(&drained, (it / (kChunk * kNKB) - 1) & 1);
+      const int kb = it - kNKB * (it / kNKB);
+      const int chunk = it / CN, cit = it - CN * chunk;   // cit = 0 restarts the chunk's accumulators
+      if (cit == 0 && chunk >= 1) mbar_wait(&drained[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
       mbar_wait(&full[s], (it / kStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t st = saddr(smem + (size_t)s * kStage);
-      const uint64_t bh = umma_desc(st + kAStage, kN / 8 * 128), bl = umma_desc(st + kAStage + kBHalf, kN / 8 * 128);
+      const int nc = T.ncols[kb];
+      const uint32_t idesc = idesc0 | ((uint32_t)(nc >> 3) << 17);
+      const uint64_t bh = umma_desc(st + kAStage, nc / 8 * 128);
+      const uint64_t bl = umma_desc(st + kAStage + nc * kKB * 4, nc / 8 * 128);
 #pragma unroll
-      for (int tau = 0; tau < 4; ++tau) {
+      for (int tau = 0; tau < 2; ++tau) {
         const uint64_t ah = umma_desc(st + (tau * 2 + 0) * kATile, 16 * 128);
         const uint64_t al = umma_desc(st + (tau * 2 + 1) * kATile, 16 * 128);
-        const uint32_t dt = tmem + tau * 128;
+        const uint32_t dt = tmem + (uint32_t)(tau * 128);
         umma_tf32(dt, ah, bh, idesc, cit > 0 ? 1u : 0u);
         umma_tf32(dt, al, bh, idesc, 1u);
         umma_tf32(dt, ah, bl, idesc, 1u);
       }
       umma_commit(&empty[s]);
-      if ((it + 1) % (kChunk * kNKB) == 0 || it + 1 == nit) umma_commit(&chunk_full);
+      if (cit == CN - 1 || it + 1 == nit) umma_commit(&chunk_full);
     }
   }
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
 TcGeo make_geo(Ctx& c) {
@@ -481,6 +620,15 @@ TcGeo make_geo(Ctx& c) {
   const int nl = (int)c.level_begin.size();
   for (int l = 0; l < kMaxLevel + 2; ++l) g.lvl_begin[l] = (int)c.level_begin[std::min(l, nl - 1)];
   return g;
+}
+
+template <typename F>
+void tc_cub(Ctx& c, F f) {
+  size_t bytes = 0;
+  FMM_CUDA(f((void*)nullptr, bytes));
+  c.cub_tmp.reserve(bytes);
+  FMM_CUDA(f((void*)c.cub_tmp.p, bytes));
+  ++c.cub_calls;
 }
 
 }  // namespace
@@ -497,61 +645,65 @@ void m2l_tc_prepare(Ctx& c) {
   const int nlev = (int)c.level_begin.size() - 1;
   if (nlev > 11) return;                                    // 10-bit Morton spread in tc_source
   const TcGeo g = make_geo(c);
+  const TcTables T = make_tables();
   cudaStream_t st = c.stream;
-  struct Cand { int lt, cls, D, R; std::vector<int> codes; std::vector<short> tbl; };
+  struct Cand { int lt, D, R; std::vector<int> codes; std::vector<short> tbl; };
   std::vector<Cand> cands;
-  c.tc_tmp.reserve(8);
+  c.tc_tmp.reserve(4);
   for (int l = 2; l < nlev; ++l) {
     const int lb = (int)c.level_begin[l], le = (int)c.level_begin[l + 1];
     if (le - lb < 1024) continue;       // small levels: the register kernel is as fast
-    // reference cells: per parity class, the first of the level with a non-empty list
-    std::vector<int> ref(8, 0x7fffffff);
-    FMM_CUDA(cudaMemcpyAsync(c.tc_tmp.p, ref.data(), 8 * sizeof(int), cudaMemcpyHostToDevice, st));
-    FMM_LAUNCH(c, k_tc_first, 148, 256, 0, c.m2l_b.p, c.m2l_e.p, lb, le, g, c.tc_tmp.p);
-    FMM_CUDA(cudaMemcpyAsync(ref.data(), c.tc_tmp.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    int ref = 0x7fffffff;
+    FMM_CUDA(cudaMemcpyAsync(c.tc_tmp.p, &ref, sizeof(int), cudaMemcpyHostToDevice, st));
+    FMM_LAUNCH(c, k_tc_first, 148, 256, 0, c.m2l_b.p, c.m2l_e.p, lb, le, c.tc_tmp.p);
+    FMM_CUDA(cudaMemcpyAsync(&ref, c.tc_tmp.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     FMM_CUDA(cudaStreamSynchronize(st));
-    for (int cls = 0; cls < 8; ++cls) {
-      if (ref[cls] == 0x7fffffff) continue;
-      int be[2];
-      FMM_CUDA(cudaMemcpyAsync(&be[0], c.m2l_b.p + ref[cls], sizeof(int), cudaMemcpyDeviceToHost, st));
-      FMM_CUDA(cudaMemcpyAsync(&be[1], c.m2l_e.p + ref[cls], sizeof(int), cudaMemcpyDeviceToHost, st));
-      FMM_CUDA(cudaStreamSynchronize(st));
-      const int D = be[1] - be[0];
-      if (D <= 0 || D > 8192) continue;
-      c.tc_codes_tmp.reserve(D);
-      FMM_LAUNCH(c, k_tc_ref_codes, 1, 256, 0, c.m2l.p, c.m2l_b.p, c.m2l_e.p, ref[cls], l, g, c.tc_codes_tmp.p);
-      Cand cd;
-      cd.lt = l;
-      cd.cls = cls;
-      cd.D = D;
-      cd.codes.resize(D);
-      FMM_CUDA(cudaMemcpyAsync(cd.codes.data(), c.tc_codes_tmp.p, sizeof(int) * D, cudaMemcpyDeviceToHost, st));
-      FMM_CUDA(cudaStreamSynchronize(st));
-      std::sort(cd.codes.begin(), cd.codes.end());
-      if (cd.codes[0] < 0 || std::adjacent_find(cd.codes.begin(), cd.codes.end()) != cd.codes.end()) continue;
-      int R = 0;
-      for (int code : cd.codes)
-        for (int a = 0; a < 3; ++a) R = std::max(R, std::abs(((code >> (14 - 7 * a)) & 127) - 64));
-      const int V = 2 * R + 1;
-      cd.R = R;
-      cd.tbl.assign((size_t)3 * V * V * V, (short)-1);
-      for (int d = 0; d < D; ++d) {
-        const int code = cd.codes[d];
-        const int dl = (code >> 21) - 1, vx = ((code >> 14) & 127) - 64, vy = ((code >> 7) & 127) - 64,
-                  vz = (code & 127) - 64;
-        cd.tbl[(((size_t)(dl + 1) * V + vx + R) * V + vy + R) * V + vz + R] = (short)d;
-      }
-      cands.push_back(std::move(cd));
+    if (ref == 0x7fffffff) continue;
+    int be[2] = {0, 0}, hq[3] = {0, 0, 0};
+    FMM_CUDA(cudaMemcpyAsync(&be[0], c.m2l_b.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&be[1], c.m2l_e.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&hq[0], c.cells.qx.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&hq[1], c.cells.qy.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&hq[2], c.cells.qz.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    const int D = be[1] - be[0];
+    if (D <= 0 || D > 8192) continue;
+    c.tc_codes_tmp.reserve(D);
+    FMM_LAUNCH(c, k_tc_ref_codes, 1, 256, 0, c.m2l.p, c.m2l_b.p, c.m2l_e.p, ref, l, g, c.tc_codes_tmp.p);
+    Cand cd;
+    cd.lt = l;
+    cd.D = D;
+    cd.codes.resize(D);
+    FMM_CUDA(cudaMemcpyAsync(cd.codes.data(), c.tc_codes_tmp.p, sizeof(int) * D, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    if (*std::min_element(cd.codes.begin(), cd.codes.end()) < 0) continue;
+    // canonical (class 0) offsets: the reference cell's, reflected from its class
+    const int rcls = (hq[0] & 1) | ((hq[1] & 1) << 1) | ((hq[2] & 1) << 2);
+    for (int& code : cd.codes) code = reflect(code, rcls);
+    std::sort(cd.codes.begin(), cd.codes.end());
+    if (std::adjacent_find(cd.codes.begin(), cd.codes.end()) != cd.codes.end()) continue;
+    int R = 0;
+    for (int code : cd.codes)
+      for (int a = 0; a < 3; ++a) R = std::max(R, std::abs(code_v(code, a)));
+    const int V = 2 * R + 1;
+    cd.R = R;
+    cd.tbl.assign((size_t)3 * V * V * V, (short)-1);
+    for (int d = 0; d < D; ++d) {
+      const int code = cd.codes[d];
+      cd.tbl[(((size_t)(code_dl(code) + 1) * V + code_v(code, 0) + R) * V + code_v(code, 1) + R) * V +
+             code_v(code, 2) + R] = (short)d;
     }
+    cands.push_back(std::move(cd));
   }
   if (cands.empty()) return;
-  // verify every cell of the candidate levels; collect the targets
+  // verify every cell of the candidate levels; collect and sort the targets
   int64_t tgt_total = 0, code_total = 0, op_total = 0;
   for (auto& cd : cands) {
     tgt_total += c.level_begin[cd.lt + 1] - c.level_begin[cd.lt];
     code_total += cd.D;
   }
   c.tc_tgt.reserve(tgt_total);
+  c.tc_tgt2.reserve(tgt_total);
   c.tc_codes.reserve(code_total);
   c.tc_cnt.reserve(cands.size());
   FMM_CUDA(cudaMemsetAsync(c.tc_cnt.p, 0, sizeof(int) * cands.size(), st));
@@ -565,7 +717,7 @@ void m2l_tc_prepare(Ctx& c) {
     FMM_CUDA(cudaMemcpyAsync(c.tc_codes.p + coff, cd.codes.data(), sizeof(int) * cd.D, cudaMemcpyHostToDevice, st));
     const unsigned blocks = (unsigned)std::min<int64_t>((le - lb + 7) / 8, 148 * 16);
     FMM_LAUNCH(c, k_tc_verify, blocks, 256, 0, c.m2l.p, c.m2l_b.p, c.m2l_e.p, lb, le, cd.lt, cd.D, g, c.tc_tbl.p, cd.R,
-               cd.cls, c.tc_skip.p, c.tc_tgt.p + toff, c.tc_cnt.p + i);
+               c.tc_skip.p, c.tc_tgt.p + toff, c.tc_cnt.p + i);
     FMM_CUDA(cudaStreamSynchronize(st));    // the table buffer is reused by the next level
     tgt_off.push_back(toff);
     code_off.push_back(coff);
@@ -575,19 +727,27 @@ void m2l_tc_prepare(Ctx& c) {
   std::vector<int> cnt(cands.size());
   FMM_CUDA(cudaMemcpyAsync(cnt.data(), c.tc_cnt.p, sizeof(int) * cands.size(), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
-  // operators of the levels that have targets
+  // Morton order of the targets (= cell index order within a level)
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const int n = cnt[i];
+    if (n <= 0) continue;
+    const int* in = c.tc_tgt.p + tgt_off[i];
+    int* outp = c.tc_tgt2.p + tgt_off[i];
+    tc_cub(c, [&](void* tmp, size_t& bytes) {
+      return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, outp, n, 0, 32, st);
+    });
+  }
   std::vector<int64_t> op_off(cands.size(), -1);
   for (size_t i = 0; i < cands.size(); ++i)
     if (cnt[i] > 0) {
       op_off[i] = op_total;
-      op_total += (int64_t)cands[i].D * kNKB * 2 * kBHalf;
+      op_total += (int64_t)cands[i].D * T.opk[kNKB];
     }
   if (op_total == 0) return;
   c.tc_op.reserve(op_total);
   for (size_t i = 0; i < cands.size(); ++i) {
     if (cnt[i] <= 0) continue;
-    FMM_LAUNCH(c, k_tc_operator, (unsigned)cands[i].D, 256, 0, c.tc_codes.p + code_off[i], cands[i].lt,
-               c.tc_op.p + op_off[i]);
+    FMM_LAUNCH(c, k_tc_operator, (unsigned)cands[i].D, 256, 0, c.tc_codes.p + code_off[i], T, c.tc_op.p + op_off[i]);
     TcLevel tl;
     tl.lt = cands[i].lt;
     tl.D = cands[i].D;
@@ -607,18 +767,25 @@ void m2l_tc_run(Ctx& c) {
   const int smem = kStages * kStage;
   FMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const TcGeo g = make_geo(c);
-  // (level, class) groups, up to kMaxTcLevels per launch
+  const TcTables T = make_tables();
+  // packed, 16-byte aligned copy of the multipoles for the row gathers
+  c.tc_mp.reserve((size_t)c.ncells * 3 * kMp);
+  {
+    const int64_t n4 = (int64_t)c.ncells * 3 * (kMp / 4);
+    FMM_LAUNCH(c, k_tc_pack, (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 32), 256, 0, c.M.p,
+               (int64_t)c.ncells, (float4*)c.tc_mp.p);
+  }
   for (size_t g0 = 0; g0 < c.tc_levels.size(); g0 += kMaxTcLevels) {
     TcArgs args{};
     int ctas = 0;
     args.nlv = (int)std::min<size_t>(kMaxTcLevels, c.tc_levels.size() - g0);
     for (int i = 0; i < args.nlv; ++i) {
       const TcLevel& tl = c.tc_levels[g0 + i];
-      args.lv[i] = {c.tc_tgt.p + tl.tgt_off, c.tc_codes.p + tl.code_off, c.tc_op.p + tl.op_off, tl.ntgt, tl.lt, tl.D,
+      args.lv[i] = {c.tc_tgt2.p + tl.tgt_off, c.tc_codes.p + tl.code_off, c.tc_op.p + tl.op_off, tl.ntgt, tl.lt, tl.D,
                     ctas};
       ctas += (int)((3 * (int64_t)tl.ntgt + kRows - 1) / kRows);
     }
-    FMM_LAUNCH(c, k_m2l_tc, (unsigned)ctas, kThreads, smem, args, g, c.M.p, c.Lc.p);
+    FMM_LAUNCH(c, k_m2l_tc, (unsigned)ctas, kThreads, smem, args, T, g, (const float4*)c.tc_mp.p, c.Lc.p);
   }
 }
 
