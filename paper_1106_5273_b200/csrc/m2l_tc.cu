@@ -467,8 +467,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
 
   if (warp < kRows / 32) {
     // ---------------------------------------------------------- producers
-    // gather: rows tid/2 + 128 h (h = 0, 1), 16-byte chunk tid & 1 of each K-block
-    const int ch = tid & 1, rr = tid >> 1;
+    // gather: rows rr + 128 h (h = 0, 1), 16-byte chunk ch of each K-block; a
+    // warp covers 16 rows x both chunks (one 32-byte sector per row) and its
+    // 16-byte stores hit 8 distinct bank quads per 8 lanes (conflict-free)
+    const int ch = (tid >> 4) & 1, rr = (tid >> 5) * 16 + (tid & 15);
     int ct[2][3];
     int comp[2], cls[2];
     const float4* src[2];
