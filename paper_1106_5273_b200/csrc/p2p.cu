@@ -100,18 +100,27 @@ struct PCells {
   const int *level, *qx, *qy, *qz, *begin, *count;
 };
 
-// accumulators of the two targets of a lane, packed (target 0, target 1)
+// Per-tile FP32 accumulators of the lane's two targets, packed (target 0, 1).
+// With w_j = alpha_j x (y_j - C) (y_j the source, C its leaf centre) the
+// pair sums factor through the source leaf (one product per pair instead of
+// the cross product alpha_j x r_ij):
+//   sum_j f alpha_j x r_ij   = (sum_j f alpha_j) x (x_i - C) - sum_j f w_j
+//   sum_j q alpha_j x r_ij   = (sum_j q alpha_j) x (x_i - C) - sum_j q w_j,   q = fp (r.alpha_i)
+// |x_i - C| and |y_j - C| are bounded by the leaf distances, so the
+// difference loses at most a few bits (the parity tests bound it).
 struct Acc2 {
-  float2 u0, u1, u2, s0, s1, s2, a0, a1, a2;
+  float2 fa0, fa1, fa2, fw0, fw1, fw2, qa0, qa1, qa2, qw0, qw1, qw2;
 };
 __device__ __forceinline__ void zero(Acc2& A) {
-  A.u0 = A.u1 = A.u2 = A.s0 = A.s1 = A.s2 = A.a0 = A.a1 = A.a2 = make_float2(0.f, 0.f);
+  A.fa0 = A.fa1 = A.fa2 = A.fw0 = A.fw1 = A.fw2 = make_float2(0.f, 0.f);
+  A.qa0 = A.qa1 = A.qa2 = A.qw0 = A.qw1 = A.qw2 = make_float2(0.f, 0.f);
 }
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
 // one source on the lane's two targets, all arithmetic packed FP32x2
 // (FFMA2/FMUL2/FADD2).  Shared-memory operands per source:
 //   q = (x', y', z', -log2(e)/(2 sigma^2))      a = (alpha/(4 pi), 1/(sqrt2 sigma))
+//   w = alpha/(4 pi) x (y - C)
 //   c = (1/(2 sqrt2 sigma), (2/sqrt pi)/(sqrt2 sigma), -(4/(3 sqrt pi))/(sqrt2 sigma)^3, 1/(2 sigma^2))  [NEAR only]
 // The stretching accumulators carry fp/(-3) (fp = f'/r); flush multiplies by -3.
 // NEAR selects the regularised kernel, else the exact singular one:
@@ -121,10 +130,12 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 //   g from erfcx with rho = r/(sqrt2 sigma) entering only through FFMA2s on r.
 template <bool NEAR>
 __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, float2 b0, float2 b1, float2 b2,
-                                      const float4 q, const float4 a, const float4 c) {
+                                      const float4 q, const float4 a, const float4 w, const float4 c) {
   const float2 rx = __fadd2_rn(x0, bc(-q.x)), ry = __fadd2_rn(x1, bc(-q.y)), rz = __fadd2_rn(x2, bc(-q.z));
   const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
-  const float2 inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
+  float2 inv;
+  if (NEAR) inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
+  else inv = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));      // rho >= 4.5: r > 0
   const float2 inv2 = __fmul2_rn(inv, inv);
   const float2 inv3 = __fmul2_rn(inv2, inv);
   float2 f, fp3;
@@ -162,26 +173,36 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
     f = inv3;
     fp3 = __fmul2_rn(inv3, inv2);
   }
-  const float2 c0 = __ffma2_rn(bc(a.y), rz, __fmul2_rn(bc(-a.z), ry));
-  const float2 c1 = __ffma2_rn(bc(a.z), rx, __fmul2_rn(bc(-a.x), rz));
-  const float2 c2 = __ffma2_rn(bc(a.x), ry, __fmul2_rn(bc(-a.y), rx));
-  A.u0 = __ffma2_rn(f, c0, A.u0); A.u1 = __ffma2_rn(f, c1, A.u1); A.u2 = __ffma2_rn(f, c2, A.u2);
-  A.a0 = __ffma2_rn(f, bc(a.x), A.a0); A.a1 = __ffma2_rn(f, bc(a.y), A.a1); A.a2 = __ffma2_rn(f, bc(a.z), A.a2);
+  A.fa0 = __ffma2_rn(f, bc(a.x), A.fa0); A.fa1 = __ffma2_rn(f, bc(a.y), A.fa1); A.fa2 = __ffma2_rn(f, bc(a.z), A.fa2);
+  A.fw0 = __ffma2_rn(f, bc(w.x), A.fw0); A.fw1 = __ffma2_rn(f, bc(w.y), A.fw1); A.fw2 = __ffma2_rn(f, bc(w.z), A.fw2);
   const float2 qq = __fmul2_rn(fp3, __ffma2_rn(rz, b2, __ffma2_rn(ry, b1, __fmul2_rn(rx, b0))));
-  A.s0 = __ffma2_rn(qq, c0, A.s0); A.s1 = __ffma2_rn(qq, c1, A.s1); A.s2 = __ffma2_rn(qq, c2, A.s2);
+  A.qa0 = __ffma2_rn(qq, bc(a.x), A.qa0); A.qa1 = __ffma2_rn(qq, bc(a.y), A.qa1); A.qa2 = __ffma2_rn(qq, bc(a.z), A.qa2);
+  A.qw0 = __ffma2_rn(qq, bc(w.x), A.qw0); A.qw1 = __ffma2_rn(qq, bc(w.y), A.qw1); A.qw2 = __ffma2_rn(qq, bc(w.z), A.qw2);
 }
 
 // per-target FP64 accumulators live in shared memory ([quantity][lane], 18
-// per lane: the two targets' u, s, sum f alpha), freeing 36 registers for
-// occupancy; each FP32 tile partial is added once per tile.
+// per lane: the two targets' u, s, sum f alpha), freeing registers for
+// occupancy; each tile's FP32 sums are combined (in FP64) once per tile:
+//   u += fa x (x_i - C) - fw,   s += -3 (qa x (x_i - C) - qw),   F += fa
 constexpr int kDQ = 18;
-__device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A) {
-  const float2 v[9] = {A.u0, A.u1, A.u2, A.s0, A.s1, A.s2, A.a0, A.a1, A.a2};
+__device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A, float2 X0, float2 X1, float2 X2,
+                                      double C0, double C1, double C2) {
 #pragma unroll
-  for (int q = 0; q < 9; ++q) {
-    const double w = q >= 3 && q < 6 ? -3.0 : 1.0;     // s carries fp/(-3)
-    sD[q][lane] += w * (double)v[q].x;
-    sD[9 + q][lane] += w * (double)v[q].y;
+  for (int h = 0; h < 2; ++h) {
+    auto pick = [&](float2 v) { return (double)(h == 0 ? v.x : v.y); };
+    const double x = pick(X0) - C0, y = pick(X1) - C1, z = pick(X2) - C2;
+    const double fa0 = pick(A.fa0), fa1 = pick(A.fa1), fa2 = pick(A.fa2);
+    const double qa0 = pick(A.qa0), qa1 = pick(A.qa1), qa2 = pick(A.qa2);
+    double* D = &sD[9 * h][lane];
+    D[0 * NT] += (fa1 * z - fa2 * y) - pick(A.fw0);
+    D[1 * NT] += (fa2 * x - fa0 * z) - pick(A.fw1);
+    D[2 * NT] += (fa0 * y - fa1 * x) - pick(A.fw2);
+    D[3 * NT] -= 3.0 * ((qa1 * z - qa2 * y) - pick(A.qw0));
+    D[4 * NT] -= 3.0 * ((qa2 * x - qa0 * z) - pick(A.qw1));
+    D[5 * NT] -= 3.0 * ((qa0 * y - qa1 * x) - pick(A.qw2));
+    D[6 * NT] += fa0;
+    D[7 * NT] += fa1;
+    D[8 * NT] += fa2;
   }
 }
 
@@ -195,6 +216,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                             unsigned long long* __restrict__ near_pairs) {
   __shared__ float4 sx[TP];   // (x', y', z', -log2(e)/(2 sigma^2))
   __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
+  __shared__ float4 sw[TP];   // alpha/(4 pi) x (y - C), C = the source leaf centre
   __shared__ float4 sc[TP];   // near-kernel constants of the source (see pair2)
   __shared__ double sD[kDQ][NT];
   const float k4 = (float)(1.0 / (4.0 * kPi));
@@ -230,13 +252,17 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
       // image shift minus the target leaf centre: sources land in the target frame
       const double shx = (img % 3 - 1) * px - cx, shy = ((img / 3) % 3 - 1) * py - cy, shz = (img / 9 - 1) * pz - cz;
+      // the source leaf centre: absolute, and in the target frame
+      const double ss = L / (double)(1 << c.level[src]);
+      const double sax = lo0 + (c.qx[src] + 0.5) * ss, say = lo1 + (c.qy[src] + 0.5) * ss, saz = lo2 + (c.qz[src] + 0.5) * ss;
+      const double C0 = sax + shx, C1 = say + shy, C2 = saz + shz;
       const int sb = c.begin[src], scnt = c.count[src];
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
         // stage the tile, far sources first: a source is "far" when it is
         // >= 4.5 sqrt2 sigma_j from the whole target leaf cube, so every pair
         // it forms has rho >= 4.5 (then 1 - g < 1e-8: the exact singular branch)
-        float4 qv[2], av[2], cv[2];
+        float4 qv[2], av[2], wv[2], cv[2];
         bool fj[2], vj[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -251,6 +277,11 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
             const float aw = sqrtf(w);
             qv[h] = make_float4(qx, qy, qz, -1.4426950408889634f * w);
             av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
+            {
+              const float ex = (float)((double)p.x - sax), ey = (float)((double)p.y - say), ez = (float)((double)p.z - saz);
+              wv[h] = make_float4(av[h].y * ez - av[h].z * ey, av[h].z * ex - av[h].x * ez, av[h].x * ey - av[h].y * ex,
+                                  0.f);
+            }
             cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx) - hst), gy = fmaxf(0.f, fabsf(qy) - hst), gz = fmaxf(0.f, fabsf(qz) - hst);
             fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
@@ -268,6 +299,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                 : nfar + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
           sx[dst] = qv[h];
           sa[dst] = av[h];
+          sw[dst] = wv[h];
           sc[dst] = cv[h];
         }
         __syncwarp();
@@ -277,10 +309,10 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
         const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
 #pragma unroll UF
-        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sa[jj]);
+        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
 #pragma unroll UN
-        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sc[jj]);
-        flush(sD, lane, A);
+        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+        flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
       }
     }
     // s += (sum_j f alpha_j) x alpha_i
