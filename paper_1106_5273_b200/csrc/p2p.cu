@@ -245,6 +245,10 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       x10 = (float)((double)p.x - cx); x11 = (float)((double)p.y - cy); x12 = (float)((double)p.z - cz);
       a1 = alp[tb + i1];
     }
+    // packed once per target pass (the target alphas live only in these pairs,
+    // so the loops need no register moves to re-pair them)
+    const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
+    const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
 #pragma unroll
     for (int q = 0; q < kDQ; ++q) sD[q][lane] = 0.0;
     for (int e = eb; e < ee; ++e) {
@@ -306,8 +310,6 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         nnear += (unsigned long long)(nj - nfar) * (unsigned long long)min(TP, tcnt - t0);
         Acc2 A;
         zero(A);
-        const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
-        const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
 #pragma unroll UF
         for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
 #pragma unroll UN
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!(h == 0 ? v0 : v1)) continue;
-      const float4 ai = h == 0 ? a0 : a1;
+      const float4 ai = h == 0 ? make_float4(B0.x, B1.x, B2.x, 0.f) : make_float4(B0.y, B1.y, B2.y, 0.f);
       const double* D = &sD[9 * h][lane];
       const double u0 = D[0 * NT], u1 = D[1 * NT], u2 = D[2 * NT], s0 = D[3 * NT], s1 = D[4 * NT], s2 = D[5 * NT];
       const double f0 = D[6 * NT], f1 = D[7 * NT], f2 = D[8 * NT];
