@@ -88,6 +88,8 @@ struct Ctx {
 
   // ---- expansions and results ----
   DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)
+  DBuf<float2> r8;                           // R_n^m of the 8 child-octant shifts (M2M, L2L)
+  int r8_order = 0;
   DBuf<double> far_M;                        // periodic super-cell multipoles
   DBuf<double2> far_part;                    // per-chunk partial far-field locals
   DBuf<float> u_near, s_near, u_far, s_far;  // sorted order, [n][3]

@@ -75,19 +75,38 @@ __global__ void k_p2m(int P, const int* __restrict__ leaf_ids, GCells c, Geo g, 
 
 // ---------------------------------------------------------------- M2M (a6)
 // M~_n^m(parent) = sum_{k,l} conj(R_k^l(d/s_p)) M~_{n-k}^{m-l}(child) 2^{-(n-k)}
-__global__ void k_m2m(int P, int64_t first, GCells c, float2* __restrict__ M) {
+// Rd of the 8 child octants: R_n^m(d) for d = (+-1/4, +-1/4, +-1/4) in parent
+// side units (octant o = (qx&1) | (qy&1) << 1 | (qz&1) << 2 of the child);
+// built once per context, shared by M2M and L2L.
+__global__ void k_octant_harmonics(int P, float2* __restrict__ R8) {
+  const int o = threadIdx.x;
+  if (o >= 8) return;
+  const float dx = 0.5f * ((float)(o & 1) - 0.5f), dy = 0.5f * ((float)((o >> 1) & 1) - 0.5f),
+              dz = 0.5f * ((float)((o >> 2) & 1) - 0.5f);
+  regular_harmonics<float>(dx, dy, dz, P, (cpx<float>*)(R8 + o * (P * (P + 1) / 2)));
+}
+
+__device__ __forceinline__ int child_octant(const GCells& c, int ch, int p) {
+  return (c.qx[ch] - 2 * c.qx[p]) | ((c.qy[ch] - 2 * c.qy[p]) << 1) | ((c.qz[ch] - 2 * c.qz[p]) << 2);
+}
+
+__global__ void k_m2m(int P, int64_t first, GCells c, const float2* __restrict__ R8, float2* __restrict__ M) {
   extern __shared__ float2 sm[];
   const int nc = P * (P + 1) / 2;
-  cpx<float>* Rd = (cpx<float>*)sm;   // [8][nc]
+  cpx<float>* Rd = (cpx<float>*)sm;             // [8][nc]
+  cpx<float>* Ms = (cpx<float>*)(sm + 8 * nc);  // [8][3][nc]: the children's multipoles
   int p = (int)(first + blockIdx.x);
   if (c.leaf[p]) return;
   int cb = c.child_begin[p], nch = c.nchild[p];
-  if ((int)threadIdx.x < nch) {
-    int ch = cb + threadIdx.x;
-    float dx = 0.5f * ((float)(c.qx[ch] - 2 * c.qx[p]) - 0.5f);
-    float dy = 0.5f * ((float)(c.qy[ch] - 2 * c.qy[p]) - 0.5f);
-    float dz = 0.5f * ((float)(c.qz[ch] - 2 * c.qz[p]) - 0.5f);
-    regular_harmonics<float>(dx, dy, dz, P, Rd + threadIdx.x * nc);
+  for (int i = threadIdx.x; i < nch * nc; i += blockDim.x) {
+    const int q = i / nc, k = i - nc * (i / nc);
+    const float2 r = R8[child_octant(c, cb + q, p) * nc + k];
+    Rd[i] = {r.x, r.y};
+  }
+  // the children are consecutive cells: one contiguous block of multipoles
+  for (int i = threadIdx.x; i < nch * 3 * nc; i += blockDim.x) {
+    const float2 v = M[(int64_t)cb * 3 * nc + i];
+    Ms[i] = {v.x, v.y};
   }
   __syncthreads();
   int o = threadIdx.x;
@@ -97,7 +116,7 @@ __global__ void k_m2m(int P, int64_t first, GCells c, float2* __restrict__ M) {
   cpx<float> acc = {0.f, 0.f};
   for (int q = 0; q < nch; ++q) {
     const cpx<float>* R = Rd + q * nc;
-    const cpx<float>* Mc = (const cpx<float>*)(M + ((int64_t)(cb + q) * 3 + comp) * nc);
+    const cpx<float>* Mc = Ms + (q * 3 + comp) * nc;
     for (int kk = n; kk >= 0; --kk) {
       int nn = n - kk;
       float sc = ldexpf(1.0f, -nn);
@@ -345,18 +364,17 @@ __global__ void k_far_reduce(int nc, int nchunk, const int* __restrict__ targets
 
 // ---------------------------------------------------------------- L2L (a10)
 // L~_a^b(child) += 2^{-(a+1)} sum_{k>=a,l} L~_k^l(parent) conj(R_{k-a}^{l-b}(d/s_p))
-__global__ void k_l2l(int P, int64_t first, GCells c, float2* __restrict__ Lc) {
+__global__ void k_l2l(int P, int64_t first, GCells c, const float2* __restrict__ R8, float2* __restrict__ Lc) {
   extern __shared__ float2 sm[];
   const int nc = P * (P + 1) / 2;
   cpx<float>* Rd = (cpx<float>*)sm;          // [nc]
   cpx<float>* Lp = (cpx<float>*)(sm + nc);   // [3][nc]
   int ch = (int)(first + blockIdx.x);
   int p = c.parent[ch];
-  if (threadIdx.x == 0) {
-    float dx = 0.5f * ((float)(c.qx[ch] - 2 * c.qx[p]) - 0.5f);
-    float dy = 0.5f * ((float)(c.qy[ch] - 2 * c.qy[p]) - 0.5f);
-    float dz = 0.5f * ((float)(c.qz[ch] - 2 * c.qz[p]) - 0.5f);
-    regular_harmonics<float>(dx, dy, dz, P, Rd);
+  const int oct = child_octant(c, ch, p);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const float2 r = R8[oct * nc + i];
+    Rd[i] = {r.x, r.y};
   }
   for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) Lp[i] = ld(Lc + (int64_t)p * 3 * nc + i);
   __syncthreads();
@@ -465,6 +483,16 @@ static Geo geo(const Ctx& c) {
           {c.per_units[0], c.per_units[1], c.per_units[2]}, c.tmax};
 }
 
+// the 8 child-octant harmonic tables (depend on p only)
+const float2* octant_r(Ctx& c) {
+  if (c.r8_order != c.P) {
+    c.r8.reserve((size_t)8 * c.nc);
+    FMM_LAUNCH(c, k_octant_harmonics, 1, 32, 0, c.P, c.r8.p);
+    c.r8_order = c.P;
+  }
+  return c.r8.p;
+}
+
 void upward_pass(Ctx& c) {
   cudaStream_t st = c.stream;
   int P = c.P, nc = c.nc;
@@ -480,7 +508,7 @@ void upward_pass(Ctx& c) {
   for (int l = nlev - 2; l >= 0; --l) {
     int64_t first = l == 0 ? 0 : c.loc_lo[l], cnt = l == 0 ? 1 : c.loc_hi[l] - c.loc_lo[l];
     if (cnt <= 0) continue;
-    FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 8 * nc, P, first, gc, c.M.p);
+    FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 32 * nc, P, first, gc, octant_r(c), c.M.p);
   }
   // root and level-1 cells (the tiles) are needed by every rank's far field
   if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc * c.level_begin[2]);
@@ -542,7 +570,7 @@ void downward_pass(Ctx& c, float* u_far, float* s_far) {
   for (int l = 1; l < nlev; ++l) {
     int64_t first = c.loc_lo[l], cnt = c.loc_hi[l] - first;
     if (cnt <= 0) continue;
-    FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, c.Lc.p);
+    FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, octant_r(c), c.Lc.p);
     FMM_LAUNCH_CHECK();
   }
   if (c.nleaves > 0 && !l2p_pass_reg(c, u_far, s_far)) {

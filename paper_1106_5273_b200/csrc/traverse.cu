@@ -130,8 +130,12 @@ void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
   c.sort_tmp.reserve(n);
   uint64_t* in = lst.p;
   uint64_t* out = c.sort_tmp.p;
+  // the target field (bits 32..58) only holds cell ids < ncells: sort no higher
+  int nb = 1;
+  while (nb < 27 && (1ll << nb) < c.ncells) ++nb;
+  const int end_bit = 32 + nb;
   cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, begin_bit, 59, c.stream);
+    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, begin_bit, end_bit, c.stream);
   });
   std::swap(lst.p, c.sort_tmp.p);
   std::swap(lst.cap, c.sort_tmp.cap);
