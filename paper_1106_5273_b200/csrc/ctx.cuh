@@ -85,6 +85,7 @@ struct Ctx {
   DBuf<float> tc_mp;                         // packed multipoles [cell][3][112] for the row gathers
   DBuf<short> tc_tbl;
   DBuf<unsigned char> tc_op;                 // pre-split operators, [level][d][K-block][hi|lo]
+  std::vector<int> tc_op_sig;                // (level, D, offsets) the operators were built for
 
   // ---- expansions and results ----
   DBuf<float2> M, Lc;                        // [ncells][3][nc], normalised (Z18)

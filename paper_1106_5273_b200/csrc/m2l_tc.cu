@@ -746,10 +746,23 @@ void m2l_tc_prepare(Ctx& c) {
       op_total += (int64_t)cands[i].D * T.opk[kNKB];
     }
   if (op_total == 0) return;
-  c.tc_op.reserve(op_total);
+  // the operators depend only on (level, canonical offsets): rebuilt only when those change
+  std::vector<int> sig;
+  for (size_t i = 0; i < cands.size(); ++i)
+    if (cnt[i] > 0) {
+      sig.push_back(cands[i].lt);
+      sig.push_back(cands[i].D);
+      sig.insert(sig.end(), cands[i].codes.begin(), cands[i].codes.end());
+    }
+  const bool rebuild = sig != c.tc_op_sig || c.tc_op.p == nullptr;
+  if (rebuild) {
+    c.tc_op.reserve(op_total);
+    c.tc_op_sig = sig;
+  }
   for (size_t i = 0; i < cands.size(); ++i) {
     if (cnt[i] <= 0) continue;
-    FMM_LAUNCH(c, k_tc_operator, (unsigned)cands[i].D, 256, 0, c.tc_codes.p + code_off[i], T, c.tc_op.p + op_off[i]);
+    if (rebuild)
+      FMM_LAUNCH(c, k_tc_operator, (unsigned)cands[i].D, 256, 0, c.tc_codes.p + code_off[i], T, c.tc_op.p + op_off[i]);
     TcLevel tl;
     tl.lt = cands[i].lt;
     tl.D = cands[i].D;
