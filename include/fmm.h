@@ -166,6 +166,18 @@ fmm_status fmm_get_expansions(const fmm_ctx* ctx, float* M, float* L);
  * of set_particles / evaluate. */
 fmm_status fmm_step(fmm_ctx* ctx, int64_t n, float* x, float* alpha, float* sigma, double dt, double nu);
 
+/* NEXT-2 (the paper's second FMM workload, velocity on a uniform
+ * lattice for spectra): the velocity of Eq. 1 at nt target points
+ * y[nt][3] that carry no vorticity, induced by the n particles (x, alpha,
+ * sigma) given here.  Evaluated as one FMM over the union of the particles and
+ * the targets (targets enter with alpha = 0, so they change no sum; their
+ * positions shape the tree exactly as extra particles would).  Writes
+ * u[nt][3] (overwrite); pointers may be device or host memory.  The context
+ * then holds the union as its particle set (as after fmm_set_particles).
+ * Single-GPU in this build.  Errors: as fmm_set_particles / fmm_evaluate. */
+fmm_status fmm_evaluate_targets(fmm_ctx* ctx, int64_t n, const float* x, const float* alpha,
+                                const float* sigma, int64_t nt, const float* y, float* u);
+
 /* Multi-GPU bootstrap: writes a fresh 128-byte ncclUniqueId into id (one rank
  * calls it and broadcasts the bytes to the others, e.g. via torch.distributed;
  * every rank then passes them as fmm_config.nccl_id).  Errors: FMM_E_NCCL. */

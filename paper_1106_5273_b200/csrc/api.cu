@@ -467,3 +467,36 @@ FMM_API fmm_status fmm_step(fmm_ctx* h, int64_t n, float* x, float* alpha, float
     FMM_CUDA(cudaStreamSynchronize(st));
   });
 }
+
+FMM_API fmm_status fmm_evaluate_targets(fmm_ctx* h, int64_t n, const float* x, const float* alpha, const float* sigma,
+                                        int64_t nt, const float* y, float* u) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (n < 0 || nt < 0 || (n > 0 && (!x || !alpha || !sigma)) || (nt > 0 && (!y || !u)))
+      throw FmmError(FMM_E_ARG, "bad arguments");
+    if (c.cfg.nranks > 1) throw FmmError(FMM_E_ARG, "fmm_evaluate_targets is single-GPU in this build");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    cudaStream_t st = c.stream;
+    const int64_t N = n + nt;
+    c.st_x.reserve(3 * N); c.st_a.reserve(3 * N); c.st_s.reserve(N);
+    c.st_u.reserve(3 * N); c.st_da.reserve(3 * N);
+    // the union: sources as given, targets with zero strength (they add nothing to any
+    // sum; their core size is irrelevant and set to 1)
+    if (n > 0) {
+      FMM_CUDA(cudaMemcpyAsync(c.st_x.p, x, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(c.st_a.p, alpha, sizeof(float) * 3 * n, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemcpyAsync(c.st_s.p, sigma, sizeof(float) * n, cudaMemcpyDefault, st));
+    }
+    if (nt > 0) {
+      FMM_CUDA(cudaMemcpyAsync(c.st_x.p + 3 * n, y, sizeof(float) * 3 * nt, cudaMemcpyDefault, st));
+      FMM_CUDA(cudaMemsetAsync(c.st_a.p + 3 * n, 0, sizeof(float) * 3 * nt, st));
+      fill_f32(c, c.st_s.p + n, nt, 1.0f);
+    }
+    set_particles_impl(c, N, c.st_x.p, c.st_a.p, c.st_s.p);
+    evaluate_impl(c, 3, c.st_u.p, c.st_da.p);
+    if (nt > 0) FMM_CUDA(cudaMemcpyAsync(u, c.st_u.p + 3 * n, sizeof(float) * 3 * nt, cudaMemcpyDefault, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -130,6 +130,7 @@ void let_exchange(Ctx& c);
 void step_stage_update(Ctx& c, const float* x, const float* a, const float* s, const float* u, const float* da,
                        int64_t n, double h, double two_nu_t, float* xo, float* ao, float* so);
 void periodic_far_pass(Ctx& c);
+void fill_f32(Ctx& c, float* p, int64_t n, float v);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g);

@@ -29,7 +29,18 @@ __global__ void k_axpy3(const float* __restrict__ x, const float* __restrict__ a
   }
 }
 
+__global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
 }  // namespace
+
+void fill_f32(Ctx& c, float* p, int64_t n, float v) {
+  if (n <= 0) return;
+  unsigned g = nblocks(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  FMM_LAUNCH(c, k_fill, g, 256, 0, p, n, v);
+}
 
 void step_stage_update(Ctx& c, const float* x, const float* a, const float* s, const float* u, const float* da,
                        int64_t n, double h, double two_nu_t, float* xo, float* ao, float* so) {

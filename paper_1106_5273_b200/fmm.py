@@ -80,9 +80,11 @@ def lib():
         L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
         L.fmm_comm_unique_id.argtypes = [vp]
         L.fmm_step.argtypes = [vp, i64, vp, vp, vp, C.c_double, C.c_double]
+        L.fmm_evaluate_targets.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
-                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id", "fmm_step"):
+                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id", "fmm_step",
+                   "fmm_evaluate_targets"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
@@ -208,6 +210,11 @@ def fmm_step(ctx, n, x, alpha, sigma, dt, nu):
     _check(ctx, lib().fmm_step(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), float(dt), float(nu)))
 
 
+def fmm_evaluate_targets(ctx, n, x, alpha, sigma, nt, y, u):
+    _check(ctx, lib().fmm_evaluate_targets(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), int(nt), _ptr(y),
+                                           _ptr(u)))
+
+
 def fmm_comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     st = lib().fmm_comm_unique_id(buf)
@@ -244,6 +251,11 @@ class FMM:
         """One midpoint-RK2 vortex step (NEXT-1); overwrites x, alpha, sigma."""
         fmm_step(self.ctx, x.shape[0], x, alpha, sigma, dt, nu)
         self.n = int(x.shape[0])
+
+    def evaluate_targets(self, x, alpha, sigma, y, u):
+        """Velocity at strength-free targets y (NEXT-2); the context then holds the union."""
+        fmm_evaluate_targets(self.ctx, x.shape[0], x, alpha, sigma, y.shape[0], y, u)
+        self.n = int(x.shape[0] + y.shape[0])
 
     def stats(self):
         return fmm_get_stats(self.ctx)
