@@ -25,8 +25,8 @@
 // the parity tests through fmm_eval_cutoff).  The pair arithmetic of the two
 // targets of a lane is packed into FP32x2 (FFMA2) with the source operands
 // broadcast, halving the issue slots per pair.  Sources whose every pair
-// with the target leaf has rho >= 4.5 (distance from the source to the leaf
-// cube >= 4.5 sqrt2 sigma_j, tested once per source while staging) are
+// with the targets has rho >= 4.5 (distance from the source to the tight box
+// of the targets >= 4.5 sqrt2 sigma_j, tested once per source while staging) are
 // compacted to the front of the tile and take the exact singular branch:
 // there 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
 #include "ctx.cuh"
@@ -249,6 +249,24 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
     // so the loops need no register moves to re-pair them)
     const float2 X0 = make_float2(x00, x10), X1 = make_float2(x01, x11), X2 = make_float2(x02, x12);
     const float2 B0 = make_float2(a0.x, a1.x), B1 = make_float2(a0.y, a1.y), B2 = make_float2(a0.z, a1.z);
+    // tight box of this pass's targets (centre bc, half extent bh): the far test
+    // below measures a source's distance to it (absent targets excluded)
+    float bc[3], bh[3];
+    {
+      const float xs[3][2] = {{x00, x10}, {x01, x11}, {x02, x12}};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        float lo = fminf(v0 ? xs[a][0] : 1e30f, v1 ? xs[a][1] : 1e30f);
+        float hi = fmaxf(v0 ? xs[a][0] : -1e30f, v1 ? xs[a][1] : -1e30f);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        bc[a] = 0.5f * (lo + hi);
+        bh[a] = 0.5f * (hi - lo) * 1.0001f + 1e-7f * hst;   // rounding margin
+      }
+    }
 #pragma unroll
     for (int q = 0; q < kDQ; ++q) sD[q][lane] = 0.0;
     for (int e = eb; e < ee; ++e) {
@@ -287,7 +305,8 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                   0.f);
             }
             cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
-            const float gx = fmaxf(0.f, fabsf(qx) - hst), gy = fmaxf(0.f, fabsf(qy) - hst), gz = fmaxf(0.f, fabsf(qz) - hst);
+            const float gx = fmaxf(0.f, fabsf(qx - bc[0]) - bh[0]), gy = fmaxf(0.f, fabsf(qy - bc[1]) - bh[1]),
+                        gz = fmaxf(0.f, fabsf(qz - bc[2]) - bh[2]);
             fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
           }
         }
