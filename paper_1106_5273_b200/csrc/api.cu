@@ -104,10 +104,31 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   c.u_near.reserve(3 * N); c.s_near.reserve(3 * N); c.u_far.reserve(3 * N); c.s_far.reserve(3 * N);
   // a5-a6 upward pass (cells of other ranks stay zero until the LET arrives)
   if (multi) FMM_CUDA(cudaMemsetAsync(c.M.p, 0, ncoef * sizeof(float2), st));
-  upward_pass(c);
-  FMM_CUDA(cudaEventRecord(c.ev[PH_UP], st));
-  // a7 traversal (once per set_particles)
-  if (!c.lists_valid) build_lists(c);
+  const bool overlap = !c.lists_valid && !multi;
+  if (overlap) {
+    // a5-a6 on the side stream while a7 (the traversal, with its host round
+    // trips between frontier rounds) runs on the main stream; joined before M2L
+    FMM_CUDA(cudaEventRecord(c.ev_fork, st));
+    FMM_CUDA(cudaStreamWaitEvent(c.stream2, c.ev_fork, 0));
+    std::swap(c.stream, c.stream2);
+    try {
+      upward_pass(c);
+      FMM_CUDA(cudaEventRecord(c.ev[PH_UP], c.stream));
+    } catch (...) {
+      std::swap(c.stream, c.stream2);
+      throw;
+    }
+    std::swap(c.stream, c.stream2);
+    build_lists(c);
+    FMM_CUDA(cudaEventRecord(c.ev_trav, st));
+    FMM_CUDA(cudaStreamWaitEvent(st, c.ev[PH_UP], 0));
+  } else {
+    upward_pass(c);
+    FMM_CUDA(cudaEventRecord(c.ev[PH_UP], st));
+    // a7 traversal (once per set_particles)
+    if (!c.lists_valid) build_lists(c);
+  }
+  c.overlapped = overlap;
   FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
   // a14 LET exchange (multipoles and bodies of the remote sources in this rank's lists)
   if (multi) {
@@ -155,7 +176,8 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   c.evaluated = true;
   fmm_stats& S = c.stats;
   S.ms_upward = ms_between(c.ev[PH_EVAL0], c.ev[PH_UP]);
-  S.ms_traverse = ms_between(c.ev[PH_UP], c.ev[PH_TRAV]);
+  // overlapped: both phases start at EVAL0 (ms_upward and ms_traverse then overlap in time)
+  S.ms_traverse = c.overlapped ? ms_between(c.ev[PH_EVAL0], c.ev_trav) : ms_between(c.ev[PH_UP], c.ev[PH_TRAV]);
   S.ms_m2l = ms_between(c.ev[PH_TRAV], c.ev[PH_M2L]);
   S.ms_p2p = ms_between(c.ev[PH_M2L], c.ev[PH_P2P]);
   S.ms_downward = ms_between(c.ev[PH_P2P], c.ev[PH_DOWN]);
@@ -215,6 +237,10 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       c.own_stream = true;
     }
     for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
+    // side stream: the upward pass runs beside the traversal (they are independent)
+    FMM_CUDA(cudaStreamCreateWithFlags(&c.stream2, cudaStreamNonBlocking));
+    FMM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    FMM_CUDA(cudaEventCreate(&c.ev_trav));
     set_expansion_smem_limits();
     FMM_CUDA(cudaGetLastError());
     comm_init(c);
@@ -229,7 +255,11 @@ FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
   Ctx& c = h->c;
   cudaSetDevice(c.cfg.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  if (c.stream2) cudaStreamSynchronize(c.stream2);
   for (int i = 0; i <= PH_N; ++i) if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.ev_trav) cudaEventDestroy(c.ev_trav);
+  if (c.stream2) cudaStreamDestroy(c.stream2);
   try { comm_destroy(c); } catch (...) {}
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
   delete h;

@@ -106,6 +106,8 @@ struct Ctx {
 
   // ---- timing ----
   cudaEvent_t ev[PH_N + 1] = {};
+  cudaEvent_t ev_fork = nullptr, ev_trav = nullptr;   // upward-pass / traversal overlap
+  bool overlapped = false;
   fmm_stats stats{};
 };
 
