@@ -77,6 +77,7 @@ constexpr int kNKB = 14;                    // K-blocks per offset (112 / 8)
 constexpr int kStages = 4;
 constexpr int kPF = TC_PF;                      // gather prefetch distance (stages)
 constexpr int kATile = 128 * kKB * 4;       // one 128-row A tile (hi or lo), bytes
+constexpr int kALbo = 16 * 128;             // A tile: stride between its two 16-byte K chunks
 constexpr int kAStage = 2 * 2 * kATile;     // 2 accumulators x (hi, lo)
 constexpr int kBMax = 2 * kN * kKB * 4;     // operator slice (hi + lo) at N = 112
 constexpr int kStage = kAStage + kBMax;
@@ -475,39 +476,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
 
   if (warp < kRows / 32) {
     // ---------------------------------------------------------- producers
-    // gather: rows rr + 128 h (h = 0, 1), 16-byte chunk ch of each K-block; a
-    // warp covers 16 rows x both chunks (one 32-byte sector per row) and its
-    // 16-byte stores hit 8 distinct bank quads per 8 lanes (conflict-free)
-    const int ch = (tid >> 4) & 1, rr = (tid >> 5) * 16 + (tid & 15);
-    int ct[2][3];
-    int comp[2], cls[2];
-    const float4* src[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int R = row0 + rr + 128 * h;
+    // gather: thread tid owns row tid (tile tid / 128) and reads its 32-byte
+    // K-block slice with one 256-bit load; a warp request covers 32 rows, i.e.
+    // ~11 targets x one 96-byte run each
+    int ct[3];
+    int comp, cls;
+    const float* src = (const float*)Mp;
+    {
+      const int R = row0 + tid;
       const int t = R < 3 * A.ntgt ? R / 3 : 0;
-      comp[h] = R < 3 * A.ntgt ? R - 3 * (R / 3) : 0;
+      comp = R < 3 * A.ntgt ? R - 3 * (R / 3) : 0;
       const int cell = A.tgt[t];
-      cls[h] = parity_class(g, cell);
-      ct[h][0] = (2 * g.qx[cell] + 1) << (kMaxLevel - A.lt);
-      ct[h][1] = (2 * g.qy[cell] + 1) << (kMaxLevel - A.lt);
-      ct[h][2] = (2 * g.qz[cell] + 1) << (kMaxLevel - A.lt);
-      src[h] = Mp;
+      cls = parity_class(g, cell);
+      ct[0] = (2 * g.qx[cell] + 1) << (kMaxLevel - A.lt);
+      ct[1] = (2 * g.qy[cell] + 1) << (kMaxLevel - A.lt);
+      ct[2] = (2 * g.qz[cell] + 1) << (kMaxLevel - A.lt);
     }
     int pf_d = -1;
-    auto load = [&](int it, float4 (&v)[2]) {
+    auto load = [&](int it, float (&v)[8]) {
       const int d = it / kNKB, kb = it - kNKB * (it / kNKB);
       if (d != pf_d) {
         pf_d = d;
         const int code = __ldg(A.codes + d);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int s = tc_source(g, A.lt, ct[h], reflect(code, cls[h]));
-          src[h] = Mp + (size_t)s * kNKB * kMpLine + comp[h] * 2;
-        }
+        const int s = tc_source(g, A.lt, ct, reflect(code, cls));
+        src = (const float*)Mp + ((size_t)s * kNKB * kMpLine + comp * 2) * 4;
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) v[h] = __ldg(src[h] + kb * kMpLine + ch);
+      asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                   : "l"(src + kb * kMpLine * 4));
     };
     // drains: thread tid owns row tid (TMEM lane quarter = warp % 4); the
     // chunk's sums are added into Lc with vector reductions (REDG.ADD.F32x2:
@@ -546,8 +542,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&drained[chunk & 1]);
     };
-    const int arow = (rr >> 3) * 128 + (rr & 7) * 16 + ch * 2048;
-    float4 buf[kPF][2];
+    const int rr = tid & 127, tau = tid >> 7;
+    const int arow = (rr >> 3) * 128 + (rr & 7) * 16;
+    float buf[kPF][8];
 #pragma unroll
     for (int u = 0; u < kPF; ++u)
       if (u < nit) load(u, buf[u]);
@@ -561,20 +558,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
           const int kb = it - kNKB * (it / kNKB);
           if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
           unsigned char* st = smem + (size_t)s * kStage;
+          const uint32_t sg = (uint32_t)T.sm[cls][kb];              // S_M of the row's class
+          float hi[8], lo[8];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t sg = (uint32_t)(T.sm[cls[h]][kb] >> (4 * ch));    // S_M of the row's class
-            float x[4] = {buf[u][h].x, buf[u][h].y, buf[u][h].z, buf[u][h].w};
-            float hi[4], lo[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              x[q] = __uint_as_float(__float_as_uint(x[q]) ^ (((sg >> q) & 1u) << 31));
-              hi[q] = tf32_hi(x[q]);
-              lo[q] = x[q] - hi[q];
-            }
-            *(float4*)(st + (h * 2 + 0) * kATile + arow) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-            *(float4*)(st + (h * 2 + 1) * kATile + arow) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          for (int q = 0; q < 8; ++q) {
+            const float x = __uint_as_float(__float_as_uint(buf[u][q]) ^ (((sg >> q) & 1u) << 31));
+            hi[q] = tf32_hi(x);
+            lo[q] = x - hi[q];
           }
+          unsigned char* ah = st + (tau * 2 + 0) * kATile + arow;
+          unsigned char* al = st + (tau * 2 + 1) * kATile + arow;
+          *(float4*)ah = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *(float4*)(ah + kALbo) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+          *(float4*)al = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          *(float4*)(al + kALbo) = make_float4(lo[4], lo[5], lo[6], lo[7]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (tid == 0) {
             const int d = it / kNKB;
