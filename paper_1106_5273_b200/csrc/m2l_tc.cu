@@ -66,7 +66,7 @@ namespace {
 #define TC_CHUNK 16
 #endif
 #ifndef TC_PF
-#define TC_PF 4
+#define TC_PF 6
 #endif
 constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
 constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
