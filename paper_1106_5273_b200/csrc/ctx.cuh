@@ -120,6 +120,7 @@ bool m2l_pass_reg(Ctx& c);
 void m2l_tc_prepare(Ctx& c);
 void m2l_tc_run(Ctx& c);
 bool l2p_pass_reg(Ctx& c, float* u_far, float* s_far);
+bool p2m_pass_reg(Ctx& c);
 void comm_init(Ctx& c);
 void comm_unique_id(void* out);
 void comm_destroy(Ctx& c);

@@ -497,7 +497,7 @@ void upward_pass(Ctx& c) {
   cudaStream_t st = c.stream;
   int P = c.P, nc = c.nc;
   GCells gc = gcells(c);
-  if (c.nleaves > 0) {
+  if (c.nleaves > 0 && !p2m_pass_reg(c)) {
     size_t sm = sizeof(float2) * (32 * nc) + sizeof(float4) * 32;
     FMM_LAUNCH(c, k_p2m, (unsigned)c.nleaves, round32(3 * nc), sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
     FMM_LAUNCH_CHECK();

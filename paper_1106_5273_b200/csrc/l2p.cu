@@ -156,6 +156,69 @@ __global__ void __launch_bounds__(64) k_l2p_reg(const int* __restrict__ leaf_ids
   }
 }
 
+// a5 P2M for p <= 10: M~_n^m(c) = sum_j alpha_j conj(R_n^m((x_j - c)/s)) per
+// component.  Thread per particle (64 per pass) with its 55 regular harmonics
+// in registers; one component at a time the products go through shared memory
+// ([particle][coefficient], stride 57 float2: conflict-free) and 55 threads sum
+// a coefficient column each, particles in order.
+template <int P>
+__global__ void __launch_bounds__(64) k_p2m_reg(const int* __restrict__ leaf_ids, LCells c, double lo0, double lo1,
+                                                double lo2, double L, const float4* __restrict__ pos,
+                                                const float4* __restrict__ alp, float2* __restrict__ M) {
+  constexpr int NC = P * (P + 1) / 2, LD = NC + (NC % 2 == 0 ? 1 : 2);
+  static_assert(LD % 2 == 1, "odd row stride in 8-byte words");
+  __shared__ float2 S[64][LD];
+  const int tid = threadIdx.x;
+  const int leaf = leaf_ids[blockIdx.x];
+  const int lev = c.level[leaf], b = c.begin[leaf], cnt = c.count[leaf];
+  const double s = L / (double)(1 << lev);
+  const double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s, cz = lo2 + (c.qz[leaf] + 0.5) * s;
+  float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  for (int j0 = 0; j0 < cnt; j0 += 64) {
+    const int i = j0 + tid;
+    const bool v = i < cnt;
+    float Rr[NC], Ri[NC];
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v) {
+      const float4 p = pos[b + i];
+      a = alp[b + i];
+      regular_unrolled<P>((float)(((double)p.x - cx) / s), (float)(((double)p.y - cy) / s),
+                          (float)(((double)p.z - cz) / s), Rr, Ri);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) Rr[k] = Ri[k] = 0.f;
+    }
+    const int nr = min(64, cnt - j0);
+#pragma unroll
+    for (int comp = 0; comp < 3; ++comp) {
+      const float ac = comp == 0 ? a.x : (comp == 1 ? a.y : a.z);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < NC; ++k) S[tid][k] = make_float2(ac * Rr[k], -ac * Ri[k]);
+      __syncthreads();
+      if (tid < NC) {
+        float2 w = acc[comp];
+        for (int r = 0; r < nr; ++r) {
+          const float2 q = S[r][tid];
+          w.x += q.x;
+          w.y += q.y;
+        }
+        acc[comp] = w;
+      }
+    }
+  }
+  if (tid < NC)
+#pragma unroll
+    for (int comp = 0; comp < 3; ++comp) M[((int64_t)leaf * 3 + comp) * NC + tid] = acc[comp];
+}
+
+template <int P>
+void launch_p2m(Ctx& c) {
+  LCells lc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
+  FMM_LAUNCH(c, k_p2m_reg<P>, (unsigned)c.nleaves, 64, 0, c.leaf_ids.p, lc, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p,
+             c.alp.p, c.M.p);
+}
+
 template <int P>
 void launch(Ctx& c, float* u_far, float* s_far) {
   LCells lc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
@@ -172,6 +235,17 @@ bool l2p_pass_reg(Ctx& c, float* u_far, float* s_far) {
     case 6: launch<6>(c, u_far, s_far); return true;
     case 8: launch<8>(c, u_far, s_far); return true;
     case 10: launch<10>(c, u_far, s_far); return true;
+    default: return false;
+  }
+}
+
+bool p2m_pass_reg(Ctx& c) {
+  if (c.nleaves == 0) return true;
+  switch (c.P) {
+    case 4: launch_p2m<4>(c); return true;
+    case 6: launch_p2m<6>(c); return true;
+    case 8: launch_p2m<8>(c); return true;
+    case 10: launch_p2m<10>(c); return true;
     default: return false;
   }
 }
