@@ -121,6 +121,8 @@ void m2l_tc_prepare(Ctx& c);
 void m2l_tc_run(Ctx& c);
 bool l2p_pass_reg(Ctx& c, float* u_far, float* s_far);
 bool p2m_pass_reg(Ctx& c);
+bool m2m_level_reg(Ctx& c, int64_t first, int64_t cnt, const float2* R8);
+bool l2l_level_reg(Ctx& c, int64_t pfirst, int64_t pcnt, int64_t clo, int64_t chi, const float2* R8);
 void comm_init(Ctx& c);
 void comm_unique_id(void* out);
 void comm_destroy(Ctx& c);

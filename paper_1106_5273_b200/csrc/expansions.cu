@@ -508,7 +508,8 @@ void upward_pass(Ctx& c) {
   for (int l = nlev - 2; l >= 0; --l) {
     int64_t first = l == 0 ? 0 : c.loc_lo[l], cnt = l == 0 ? 1 : c.loc_hi[l] - c.loc_lo[l];
     if (cnt <= 0) continue;
-    FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 32 * nc, P, first, gc, octant_r(c), c.M.p);
+    if (!m2m_level_reg(c, first, cnt, octant_r(c)))
+      FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 32 * nc, P, first, gc, octant_r(c), c.M.p);
   }
   // root and level-1 cells (the tiles) are needed by every rank's far field
   if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc * c.level_begin[2]);
@@ -570,7 +571,9 @@ void downward_pass(Ctx& c, float* u_far, float* s_far) {
   for (int l = 1; l < nlev; ++l) {
     int64_t first = c.loc_lo[l], cnt = c.loc_hi[l] - first;
     if (cnt <= 0) continue;
-    FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, octant_r(c), c.Lc.p);
+    if (!l2l_level_reg(c, c.level_begin[l - 1], c.level_begin[l] - c.level_begin[l - 1], first, first + cnt,
+                       octant_r(c)))
+      FMM_LAUNCH(c, k_l2l, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 4 * nc, P, first, gc, octant_r(c), c.Lc.p);
     FMM_LAUNCH_CHECK();
   }
   if (c.nleaves > 0 && !l2p_pass_reg(c, u_far, s_far)) {
