@@ -183,8 +183,7 @@ __device__ __forceinline__ int tc_source(const TcGeo& g, int lt, const I (&ct)[3
   for (int a = 0; a < 3; ++a) {
     const int P = (int)g.per[a];
     int cs = (int)ct[a] - code_v(code, a) * (1 << (kMaxLevel - lf));
-    cs %= P;
-    if (cs < 0) cs += P;
+    cs &= P - 1;                                   // periods are powers of two (checked on the host)
     q[a] = (uint32_t)(((cs >> (kMaxLevel - ls)) - 1) >> 1);
   }
   return g.lvl_begin[ls] + (int)(spread3_32(q[0]) | (spread3_32(q[1]) << 1) | (spread3_32(q[2]) << 2));
@@ -203,9 +202,9 @@ __device__ __forceinline__ int entry_code(const TcGeo& g, int lt, const long lon
   for (int a = 0; a < 3; ++a) {
     const long long cs = (long long)(2 * qs[a] + 1) << (kMaxLevel - ls);
     const long long d = ct[a] - cs - (long long)im[a] * g.per[a];
-    const long long u = 1ll << (kMaxLevel - lf);
-    if (d % u != 0) return -1;
-    const long long v = d / u;
+    const int sh = kMaxLevel - lf;                  // Delta is a multiple of 2^sh for a valid entry
+    if (d & ((1ll << sh) - 1)) return -1;
+    const long long v = d >> sh;
     if (v < -63 || v > 63) return -1;
     code |= (int)(v + 64) << (14 - 7 * a);
   }
@@ -649,6 +648,8 @@ void m2l_tc_prepare(Ctx& c) {
   c.tc_skip.reserve(std::max<int64_t>(c.ncells, 1));
   FMM_CUDA(cudaMemsetAsync(c.tc_skip.p, 0, std::max<int64_t>(c.ncells, 1), c.stream));
   if (c.cfg.m2l_path != 0 || c.P != kTcP || c.nm2l == 0) return;
+  for (int a = 0; a < 3; ++a)
+    if (c.per_units[a] & (c.per_units[a] - 1)) return;       // tc_source wraps with a mask
   const int nlev = (int)c.level_begin.size() - 1;
   if (nlev > 11) return;                                    // 10-bit Morton spread in tc_source
   const TcGeo g = make_geo(c);
