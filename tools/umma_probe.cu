@@ -30,7 +30,7 @@ __device__ inline uint64_t desc_kmajor(uint32_t saddr, int R) {
 __device__ inline float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 __global__ void probe(const float* A, const float* B, float* D1, float* D3, float* Dacc, int racc, long long* cyc,
-                      int reps) {
+                      int reps, int raw_hi) {
   extern __shared__ __align__(1024) uint8_t sm[];
   float* Ah = (float*)sm;                       // M x K
   float* Al = (float*)(sm + M * K * 4);
@@ -42,7 +42,7 @@ __global__ void probe(const float* A, const float* B, float* D1, float* D3, floa
   for (int i = tid; i < M * K; i += blockDim.x) {
     const int r = i / K, k = i % K;
     const float v = A[i], h = tf32_hi(v);
-    *(float*)((uint8_t*)Ah + off_kmajor(r, k, M)) = h;
+    *(float*)((uint8_t*)Ah + off_kmajor(r, k, M)) = raw_hi ? v : h;   // raw: the tensor core reads x as TF32 itself
     *(float*)((uint8_t*)Al + off_kmajor(r, k, M)) = v - h;
   }
   for (int i = tid; i < N * K; i += blockDim.x) {
@@ -162,7 +162,8 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int reps = 2000;
   const int racc = argc > 1 ? atoi(argv[1]) : 1000;
-  probe<<<1, 128, smem>>>(dA, dB, d1, d3, dacc, racc, dc, reps);
+  const int raw_hi = argc > 2 ? atoi(argv[2]) : 0;
+  probe<<<1, 128, smem>>>(dA, dB, d1, d3, dacc, racc, dc, reps, raw_hi);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
   std::vector<float> D1(M * N), D3(M * N);
