@@ -186,23 +186,40 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
 //   u += fa x (x_i - C) - fw,   s += -3 (qa x (x_i - C) - qw),   F += fa
 constexpr int kDQ = 18;
 __device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A, float2 X0, float2 X1, float2 X2,
-                                      double C0, double C1, double C2) {
+                                      float C0, float C1, float C2) {
+  // tile sums in FP32 (packed over the two targets), then into the FP64 accumulators
+  const float2 x = __fadd2_rn(X0, bc(-C0)), y = __fadd2_rn(X1, bc(-C1)), z = __fadd2_rn(X2, bc(-C2));
+  const float2 u0 = __fadd2_rn(__ffma2_rn(A.fa1, z, __fmul2_rn(A.fa2, __fmul2_rn(y, bc(-1.f)))), __fmul2_rn(A.fw0, bc(-1.f)));
+  const float2 u1 = __fadd2_rn(__ffma2_rn(A.fa2, x, __fmul2_rn(A.fa0, __fmul2_rn(z, bc(-1.f)))), __fmul2_rn(A.fw1, bc(-1.f)));
+  const float2 u2 = __fadd2_rn(__ffma2_rn(A.fa0, y, __fmul2_rn(A.fa1, __fmul2_rn(x, bc(-1.f)))), __fmul2_rn(A.fw2, bc(-1.f)));
+  const float2 s0 = __fadd2_rn(__ffma2_rn(A.qa1, z, __fmul2_rn(A.qa2, __fmul2_rn(y, bc(-1.f)))), __fmul2_rn(A.qw0, bc(-1.f)));
+  const float2 s1 = __fadd2_rn(__ffma2_rn(A.qa2, x, __fmul2_rn(A.qa0, __fmul2_rn(z, bc(-1.f)))), __fmul2_rn(A.qw1, bc(-1.f)));
+  const float2 s2 = __fadd2_rn(__ffma2_rn(A.qa0, y, __fmul2_rn(A.qa1, __fmul2_rn(x, bc(-1.f)))), __fmul2_rn(A.qw2, bc(-1.f)));
+  const float2 v[9] = {u0, u1, u2, s0, s1, s2, A.fa0, A.fa1, A.fa2};
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    auto pick = [&](float2 v) { return (double)(h == 0 ? v.x : v.y); };
-    const double x = pick(X0) - C0, y = pick(X1) - C1, z = pick(X2) - C2;
-    const double fa0 = pick(A.fa0), fa1 = pick(A.fa1), fa2 = pick(A.fa2);
-    const double qa0 = pick(A.qa0), qa1 = pick(A.qa1), qa2 = pick(A.qa2);
-    double* D = &sD[9 * h][lane];
-    D[0 * NT] += (fa1 * z - fa2 * y) - pick(A.fw0);
-    D[1 * NT] += (fa2 * x - fa0 * z) - pick(A.fw1);
-    D[2 * NT] += (fa0 * y - fa1 * x) - pick(A.fw2);
-    D[3 * NT] -= 3.0 * ((qa1 * z - qa2 * y) - pick(A.qw0));
-    D[4 * NT] -= 3.0 * ((qa2 * x - qa0 * z) - pick(A.qw1));
-    D[5 * NT] -= 3.0 * ((qa0 * y - qa1 * x) - pick(A.qw2));
-    D[6 * NT] += fa0;
-    D[7 * NT] += fa1;
-    D[8 * NT] += fa2;
+  for (int q = 0; q < 9; ++q) {
+    const double w = q >= 3 && q < 6 ? -3.0 : 1.0;     // s carries fp/(-3)
+    sD[q][lane] += w * (double)v[q].x;
+    sD[9 + q][lane] += w * (double)v[q].y;
+  }
+}
+
+// leaf-local FP32 source data (a12 staging, once per evaluate): for every
+// particle of every leaf, (x - c_leaf) rounded from double, and 1/(2 sigma^2)
+__global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t ncells, double lo0, double lo1,
+                             double lo2, double L, const float4* __restrict__ pos, float4* __restrict__ posl) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t cell = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; cell < ncells;
+       cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (!leaf[cell]) continue;
+    const double s = L / (double)(1 << c.level[cell]);
+    const double cx = lo0 + (c.qx[cell] + 0.5) * s, cy = lo1 + (c.qy[cell] + 0.5) * s, cz = lo2 + (c.qz[cell] + 0.5) * s;
+    const int b = c.begin[cell], n = c.count[cell];
+    for (int i = lane; i < n; i += 32) {
+      const float4 p = pos[b + i];
+      posl[b + i] = make_float4((float)((double)p.x - cx), (float)((double)p.y - cy), (float)((double)p.z - cz),
+                                1.0f / (2.0f * p.w * p.w));
+    }
   }
 }
 
@@ -211,7 +228,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             double px, double py, double pz,
-                                            const float4* __restrict__ pos, const float4* __restrict__ alp,
+                                            const float4* __restrict__ posl, const float4* __restrict__ alp,
                                             float* __restrict__ un, float* __restrict__ sn,
                                             unsigned long long* __restrict__ near_pairs) {
   __shared__ float4 sx[TP];   // (x', y', z', -log2(e)/(2 sigma^2))
@@ -236,13 +253,13 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
     float x00 = 1e4f, x01 = 1e4f, x02 = 1e4f, x10 = 1e4f, x11 = 1e4f, x12 = 1e4f;
     float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
     if (v0) {
-      const float4 p = pos[tb + i0];
-      x00 = (float)((double)p.x - cx); x01 = (float)((double)p.y - cy); x02 = (float)((double)p.z - cz);
+      const float4 p = posl[tb + i0];                // leaf-local = target-frame coordinates
+      x00 = p.x; x01 = p.y; x02 = p.z;
       a0 = alp[tb + i0];
     }
     if (v1) {
-      const float4 p = pos[tb + i1];
-      x10 = (float)((double)p.x - cx); x11 = (float)((double)p.y - cy); x12 = (float)((double)p.z - cz);
+      const float4 p = posl[tb + i1];
+      x10 = p.x; x11 = p.y; x12 = p.z;
       a1 = alp[tb + i1];
     }
     // packed once per target pass (the target alphas live only in these pairs,
@@ -272,12 +289,12 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
     for (int e = eb; e < ee; ++e) {
       const uint64_t ent = lst[e];
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
-      // image shift minus the target leaf centre: sources land in the target frame
-      const double shx = (img % 3 - 1) * px - cx, shy = ((img / 3) % 3 - 1) * py - cy, shz = (img / 9 - 1) * pz - cz;
-      // the source leaf centre: absolute, and in the target frame
+      // the source leaf centre in the target frame (image shift included), in
+      // double then rounded: sources are y' + C with y' their leaf-local coordinates
       const double ss = L / (double)(1 << c.level[src]);
-      const double sax = lo0 + (c.qx[src] + 0.5) * ss, say = lo1 + (c.qy[src] + 0.5) * ss, saz = lo2 + (c.qz[src] + 0.5) * ss;
-      const double C0 = sax + shx, C1 = say + shy, C2 = saz + shz;
+      const float C0 = (float)(lo0 + (c.qx[src] + 0.5) * ss + (img % 3 - 1) * px - cx);
+      const float C1 = (float)(lo1 + (c.qy[src] + 0.5) * ss + ((img / 3) % 3 - 1) * py - cy);
+      const float C2 = (float)(lo2 + (c.qz[src] + 0.5) * ss + (img / 9 - 1) * pz - cz);
       const int sb = c.begin[src], scnt = c.count[src];
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
@@ -292,18 +309,15 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           vj[h] = j < scnt;
           fj[h] = false;
           if (vj[h]) {
-            const float4 p = pos[sb + j];
+            const float4 p = posl[sb + j];               // (y - C, 1/(2 sigma^2))
             const float4 a = alp[sb + j];
-            const float w = 1.0f / (2.0f * p.w * p.w);
-            const float qx = (float)((double)p.x + shx), qy = (float)((double)p.y + shy), qz = (float)((double)p.z + shz);
+            const float w = p.w;
+            const float qx = p.x + C0, qy = p.y + C1, qz = p.z + C2;
             const float aw = sqrtf(w);
             qv[h] = make_float4(qx, qy, qz, -1.4426950408889634f * w);
             av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
-            {
-              const float ex = (float)((double)p.x - sax), ey = (float)((double)p.y - say), ez = (float)((double)p.z - saz);
-              wv[h] = make_float4(av[h].y * ez - av[h].z * ey, av[h].z * ex - av[h].x * ez, av[h].x * ey - av[h].y * ex,
-                                  0.f);
-            }
+            wv[h] = make_float4(av[h].y * p.z - av[h].z * p.y, av[h].z * p.x - av[h].x * p.z,
+                                av[h].x * p.y - av[h].y * p.x, 0.f);
             cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx - bc[0]) - bh[0]), gy = fmaxf(0.f, fabsf(qy - bc[1]) - bh[1]),
                         gz = fmaxf(0.f, fabsf(qz - bc[2]) - bh[2]);
@@ -371,8 +385,11 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   // 16 blocks/SM (128 registers), far loop unrolled 4x, near 2x: the best of
   // the occupancy/unroll sweep on C3 (tools/p2p_sweep.py history)
+  c.posl.reserve(std::max<int64_t>(c.ntot, 1));
+  FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
+             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p);
   FMM_LAUNCH(c, (k_p2p<16, 4, 2>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
-             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.pos.p, c.alp.p, u_near, s_near,
+             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
              c.dnear.p);
 }
 
