@@ -68,6 +68,9 @@ namespace {
 #ifndef TC_PF
 #define TC_PF 6
 #endif
+#ifndef TC_DIAG
+#define TC_DIAG 0   // development only (tools/build_variant.py): 1 = every row reads its own cell, 2 = no gathers
+#endif
 constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
 constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
 constexpr int kRows = 256;                  // rows (target, component) per CTA
@@ -497,9 +500,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
       if (d != pf_d) {
         pf_d = d;
         const int code = __ldg(A.codes + d);
+#if TC_DIAG == 1
+        const int s = A.tgt[(row0 + tid) < 3 * A.ntgt ? (row0 + tid) / 3 : 0] + 0 * code;   // diagnostic: no gather spread
+#else
         const int s = tc_source(g, A.lt, ct, reflect(code, cls));
+#endif
         src = (const float*)Mp + ((size_t)s * kNKB * kMpLine + comp * 2) * 4;
       }
+#if TC_DIAG == 2
+      for (int q = 0; q < 8; ++q) v[q] = __int_as_float(kb + q);   // diagnostic: no loads
+      return;
+#endif
       asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                    : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
                    : "l"(src + kb * kMpLine * 4));

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmm_b200.so")
+LIB_PATH = os.environ.get("FMM_LIB") or os.path.join(_HERE, "libfmm_b200.so")   # FMM_LIB: development variants (tools/build_variant.py)
 
 FMM_OK, FMM_E_ARG, FMM_E_NONFINITE, FMM_E_SIGMA, FMM_E_STATE, FMM_E_OOM, FMM_E_CUDA, FMM_E_NCCL, FMM_E_INTERNAL = range(9)
 STATUS_NAMES = ["FMM_OK", "FMM_E_ARG", "FMM_E_NONFINITE", "FMM_E_SIGMA", "FMM_E_STATE", "FMM_E_OOM",
