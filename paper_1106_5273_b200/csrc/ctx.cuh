@@ -59,7 +59,6 @@ struct Ctx {
   DBuf<float> stage_x, stage_a, stage_s;    // host-input staging
   DBuf<float4> pos_tmp, pos, alp;           // sorted: (x,y,z,sigma), (alpha,0)
   DBuf<float4> posl;                         // leaf-local (x - c_leaf, 1/(2 sigma^2)) for P2P staging
-  DBuf<float4> psa, psw, psc;                // P2P source constants (target independent, see p2p.cu)
   DBuf<uint64_t> keys_tmp, keys;
   DBuf<uint32_t> idx_tmp, idx;               // idx[i] = caller index of sorted slot i
   DBuf<unsigned char> cub_tmp;

@@ -205,16 +205,10 @@ __device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A,
 }
 
 // leaf-local FP32 source data (a12 staging, once per evaluate): for every
-// particle of every leaf, (x - c_leaf) rounded from double and 1/(2 sigma^2),
-// and the target-independent source constants the pair kernel reads (pair2):
-//   sa = (alpha/(4 pi), 1/(sqrt2 sigma)),  sw = alpha/(4 pi) x (x - c_leaf),
-//   sc = (1/(2 sqrt2 sigma), (2/sqrt pi)/(sqrt2 sigma), -(4/(3 sqrt pi))/(sqrt2 sigma)^3, 1/(2 sigma^2))
+// particle of every leaf, (x - c_leaf) rounded from double, and 1/(2 sigma^2)
 __global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t ncells, double lo0, double lo1,
-                             double lo2, double L, const float4* __restrict__ pos, const float4* __restrict__ alp,
-                             float4* __restrict__ posl, float4* __restrict__ psa, float4* __restrict__ psw,
-                             float4* __restrict__ psc) {
+                             double lo2, double L, const float4* __restrict__ pos, float4* __restrict__ posl) {
   const int lane = threadIdx.x & 31;
-  const float k4 = (float)(1.0 / (4.0 * kPi));
   for (int64_t cell = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; cell < ncells;
        cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     if (!leaf[cell]) continue;
@@ -223,15 +217,8 @@ __global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t nce
     const int b = c.begin[cell], n = c.count[cell];
     for (int i = lane; i < n; i += 32) {
       const float4 p = pos[b + i];
-      const float4 a = alp[b + i];
-      const float4 q = make_float4((float)((double)p.x - cx), (float)((double)p.y - cy), (float)((double)p.z - cz),
-                                   1.0f / (2.0f * p.w * p.w));
-      posl[b + i] = q;
-      const float w = q.w, aw = sqrtf(w);
-      const float4 av = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
-      psa[b + i] = av;
-      psw[b + i] = make_float4(av.y * q.z - av.z * q.y, av.z * q.x - av.x * q.z, av.x * q.y - av.y * q.x, 0.f);
-      psc[b + i] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
+      posl[b + i] = make_float4((float)((double)p.x - cx), (float)((double)p.y - cy), (float)((double)p.z - cz),
+                                1.0f / (2.0f * p.w * p.w));
     }
   }
 }
@@ -242,8 +229,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                             PCells c, double lo0, double lo1, double lo2, double L,
                                             double px, double py, double pz,
                                             const float4* __restrict__ posl, const float4* __restrict__ alp,
-                                            const float4* __restrict__ psa, const float4* __restrict__ psw,
-                                            const float4* __restrict__ psc, float* __restrict__ un, float* __restrict__ sn,
+                                            float* __restrict__ un, float* __restrict__ sn,
                                             unsigned long long* __restrict__ near_pairs) {
   __shared__ float4 sx[TP];   // (x', y', z', -log2(e)/(2 sigma^2))
   __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
@@ -251,6 +237,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
   __shared__ float4 sc[TP];   // near-kernel constants of the source (see pair2)
   __shared__ double sD[kDQ][NT];
   __shared__ float2 sB[3][NT];   // the lane's target alpha pairs (reloaded as aligned register pairs)
+  const float k4 = (float)(1.0 / (4.0 * kPi));
   const int lane = threadIdx.x;
   const int leaf = leaf_ids[blockIdx.x];
   const int lev = c.level[leaf], tb = c.begin[leaf], tcnt = c.count[leaf];
@@ -327,12 +314,15 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           fj[h] = false;
           if (vj[h]) {
             const float4 p = posl[sb + j];               // (y - C, 1/(2 sigma^2))
-            av[h] = psa[sb + j];
-            wv[h] = psw[sb + j];
-            cv[h] = psc[sb + j];
+            const float4 a = alp[sb + j];
             const float w = p.w;
             const float qx = p.x + C0, qy = p.y + C1, qz = p.z + C2;
+            const float aw = sqrtf(w);
             qv[h] = make_float4(qx, qy, qz, -1.4426950408889634f * w);
+            av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
+            wv[h] = make_float4(av[h].y * p.z - av[h].z * p.y, av[h].z * p.x - av[h].x * p.z,
+                                av[h].x * p.y - av[h].y * p.x, 0.f);
+            cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx - bc[0]) - bh[0]), gy = fmaxf(0.f, fabsf(qy - bc[1]) - bh[1]),
                         gz = fmaxf(0.f, fabsf(qz - bc[2]) - bh[2]);
             fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
@@ -407,15 +397,11 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   // 16 blocks/SM (128 registers), far loop unrolled 4x, near 2x: the best of
   // the occupancy/unroll sweep on C3 (tools/p2p_sweep.py history)
-  const int64_t np = std::max<int64_t>(c.ntot, 1);
-  c.posl.reserve(np);
-  c.psa.reserve(np);
-  c.psw.reserve(np);
-  c.psc.reserve(np);
+  c.posl.reserve(std::max<int64_t>(c.ntot, 1));
   FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
-             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.alp.p, c.posl.p, c.psa.p, c.psw.p, c.psc.p);
+             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p);
   FMM_LAUNCH(c, (k_p2p<16, 4, 2>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
-             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, c.psa.p, c.psw.p, c.psc.p, u_near, s_near,
+             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
              c.dnear.p);
 }
 
