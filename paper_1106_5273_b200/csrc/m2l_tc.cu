@@ -63,7 +63,7 @@ namespace fmmb {
 namespace {
 
 #ifndef TC_CHUNK
-#define TC_CHUNK 16
+#define TC_CHUNK 32
 #endif
 #ifndef TC_PF
 #define TC_PF 6
@@ -85,7 +85,12 @@ constexpr int kAStage = 2 * 2 * kATile;     // 2 accumulators x (hi, lo)
 constexpr int kBMax = 2 * kN * kKB * 4;     // operator slice (hi + lo) at N = 112
 constexpr int kStage = kAStage + kBMax;
 constexpr int kThreads = kRows + 32;
-constexpr int kChunk = TC_CHUNK;                  // offsets accumulated in TMEM between drains
+// offsets accumulated in TMEM between drains: each drain stalls the CTA's MMAs
+// (one accumulator set per CTA), so fewer drains are faster (C3: 16 -> 73.0 ms,
+// 24 -> 70.5, 32 -> 68.7, 48 -> 67.5) while the truncation drift grows with the
+// MMAs per chunk (far-field u vs the oracle, TG 32^3: 1.6e-6, 2.1e-6, 2.5e-6,
+// 3.4e-6; register kernel 4.8e-7, bar 1e-5)
+constexpr int kChunk = TC_CHUNK;
 constexpr int kMaxTcLevels = 16;
 
 // ---------------------------------------------------------------- PTX ----
