@@ -72,9 +72,10 @@ typedef struct {
   int32_t  traversal;            /* 0 = MAC-first (default), 1 = leaf-first (Z11)      */
   int32_t  device;               /* CUDA ordinal                                       */
   void*    stream;               /* cudaStream_t for all work; NULL = library-owned    */
-  int32_t  rank, nranks;         /* nranks in {1,2,4,8}; rank r owns the particles whose
-                                    Morton keys lie in top octants [8r/P, 8(r+1)/P)
-                                    (each rank passes only those, else FMM_E_ARG) */
+  int32_t  rank, nranks;         /* partition = 0: nranks in {1,2,4,8} and rank r owns the
+                                    particles whose Morton keys lie in top octants
+                                    [8r/P, 8(r+1)/P) (each rank passes only those,
+                                    else FMM_E_ARG); partition = 1: 1 <= nranks <= 8   */
   const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1 (all ranks
                                     pass the same id, e.g. broadcast by torch.distributed) */
   int32_t  tiles[3];             /* periodic domain of tiles[d] cubes of side box_len per
@@ -84,6 +85,15 @@ typedef struct {
   int32_t  m2l_path;             /* 0 (default): tensor-core M2L (tcgen05, 3xTF32) on the
                                     levels whose cells share one offset set, register
                                     kernel elsewhere; 1: register (CUDA-core) kernel only */
+  int32_t  partition;            /* multi-GPU ownership (tiles == (1,1,1) only):
+                                    0 (default): the caller's octant blocks (above);
+                                    1: balanced -- every rank passes ANY of the particles;
+                                    set_particles sorts all keys globally, cuts the Morton
+                                    curve into nranks equal-count ranges moved to the
+                                    nearest leaf boundary (load balancing),
+                                    redistributes the particles to their owners (NCCL)
+                                    and evaluate returns every rank its own particles'
+                                    results in its caller order                          */
 } fmm_config;
 
 /* Per-phase device times of the last set_particles / evaluate (CUDA events on
@@ -108,6 +118,8 @@ typedef struct {
   int64_t  let_cells, let_leaves;           /* remote multipoles / leaves received         */
   double   ms_let;                          /* exchange time (CUDA events, incl. requests) */
   int64_t  m2l_tc_list;                     /* M2L entries evaluated on the tensor cores    */
+  int64_t  own_begin, own_count;            /* global sorted positions this rank owns        */
+  int64_t  redist_bytes;                    /* partition = 1: particle bytes sent by set_particles */
 } fmm_stats;
 
 /* Fill cfg with the defaults listed above. */

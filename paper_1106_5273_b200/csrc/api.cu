@@ -31,6 +31,34 @@ __global__ void k_finalize(const uint32_t* __restrict__ idx, int64_t n, int64_t 
   }
 }
 
+// balanced partition: owned results in receive order (6 floats: u, s), sent back
+// to the ranks the particles came from; there they land in the caller's order
+__global__ void k_ret_pack(const int* __restrict__ gp, int64_t m, int parts, const float* __restrict__ un,
+                           const float* __restrict__ sn, const float* __restrict__ uf, const float* __restrict__ sf,
+                           float* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = 3 * (int64_t)gp[k];
+    for (int d = 0; d < 3; ++d) {
+      float uu = 0.f, ss = 0.f;
+      if (parts & 1) { uu += un[g + d]; ss += sn[g + d]; }
+      if (parts & 2) { uu += uf[g + d]; ss += sf[g + d]; }
+      out[6 * k + d] = uu;
+      out[6 * k + 3 + d] = ss;
+    }
+  }
+}
+
+__global__ void k_ret_unpack(const float* __restrict__ in, const uint32_t* __restrict__ idx, int64_t n,
+                             float* __restrict__ u, float* __restrict__ s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = 3 * (int64_t)idx[i];
+    for (int d = 0; d < 3; ++d) {
+      u[o + d] = in[6 * i + d];
+      s[o + d] = in[6 * i + 3 + d];
+    }
+  }
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -55,8 +83,10 @@ void check_config(const fmm_config& c) {
   if (c.images > 0 && !(c.box_len > 0.0 && std::isfinite(c.box_len))) throw FmmError(FMM_E_ARG, "box_len must be > 0");
   if (c.traversal != 0 && c.traversal != 1) throw FmmError(FMM_E_ARG, "traversal must be 0 or 1");
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) throw FmmError(FMM_E_ARG, "bad rank/nranks");
-  if (c.nranks != 1 && c.nranks != 2 && c.nranks != 4 && c.nranks != 8)
-    throw FmmError(FMM_E_ARG, "nranks must be 1, 2, 4 or 8 (ranks own top-level Morton octants)");
+  if (c.partition != 0 && c.partition != 1) throw FmmError(FMM_E_ARG, "partition must be 0 or 1");
+  if (c.partition == 0 && c.nranks != 1 && c.nranks != 2 && c.nranks != 4 && c.nranks != 8)
+    throw FmmError(FMM_E_ARG, "nranks must be 1, 2, 4 or 8 (ranks own top-level Morton octants); see partition = 1");
+  if (c.nranks > 8) throw FmmError(FMM_E_ARG, "nranks must be <= 8 (one NVLink node)");
   if (c.nranks > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "multi-GPU needs the periodic mode (images >= 1)");
   int tp = 1;
   for (int d = 0; d < 3; ++d) {
@@ -65,6 +95,7 @@ void check_config(const fmm_config& c) {
   }
   if (tp > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "tiles need the periodic mode");
   if (tp > 1 && c.nranks != 1 && c.nranks != tp) throw FmmError(FMM_E_ARG, "with tiles, nranks must equal their product");
+  if (tp > 1 && c.partition != 0) throw FmmError(FMM_E_ARG, "tiles own whole cubes: partition must be 0");
 }
 
 template <typename F>
@@ -163,8 +194,31 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   if (hs) { c.stage_ds.reserve(3 * n); ds = c.stage_ds.p; }
   unsigned g = nblocks(n, 256);
   if (g > 148 * 16) g = 148 * 16;
-  if (n > 0)
+  if (c.balanced) {
+    const int P = c.cfg.nranks, R = c.cfg.rank;
+    c.ret_send.reserve(6 * std::max<int64_t>(c.nown, 1));
+    c.ret_recv.reserve(6 * std::max<int64_t>(n, 1));
+    if (c.nown > 0)
+      FMM_LAUNCH(c, k_ret_pack, nblocks(c.nown, 256), 256, 0, c.recv_gp.p, c.nown, parts, c.u_near.p, c.s_near.p,
+                 c.u_far.p, c.s_far.p, c.ret_send.p);
+    std::vector<int64_t> soff(P, 0), sb(P, 0), roff(P, 0), rb(P, 0);
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < P; ++q) {              // the reverse of set_particles' redistribution
+      soff[q] = 24 * so;
+      roff[q] = 24 * ro;
+      sb[q] = q == R ? 0 : 24 * c.red_rcnt[q];
+      rb[q] = q == R ? 0 : 24 * c.red_scnt[q];
+      so += c.red_rcnt[q];
+      ro += c.red_scnt[q];
+    }
+    if (c.red_rcnt[R] > 0)
+      FMM_CUDA(cudaMemcpyAsync((char*)c.ret_recv.p + roff[R], (const char*)c.ret_send.p + soff[R], 24 * c.red_rcnt[R],
+                               cudaMemcpyDeviceToDevice, st));
+    alltoallv_bytes(c, c.ret_send.p, soff, sb, c.ret_recv.p, roff, rb);
+    if (n > 0) FMM_LAUNCH(c, k_ret_unpack, g, 256, 0, c.ret_recv.p, c.idx.p, n, du, ds);
+  } else if (n > 0) {
     FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, c.off, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
+  }
   FMM_LAUNCH_CHECK();
   if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
   if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
@@ -209,6 +263,7 @@ FMM_API void fmm_config_default(fmm_config* cfg) {
   cfg->nccl_id = nullptr;
   cfg->tiles[0] = cfg->tiles[1] = cfg->tiles[2] = 1;
   cfg->m2l_path = 0;
+  cfg->partition = 0;
 }
 
 FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
@@ -337,6 +392,9 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->launches = c.launches;
   s->p2p_near_pairs = c.p2p_near_pairs;
   s->ntot = c.ntot;
+  s->own_begin = c.off;
+  s->own_count = c.nown;
+  s->redist_bytes = c.redist_bytes;
   s->let_bytes_sent = c.let_bytes_sent;
   s->let_bytes_recv = c.let_bytes_recv;
   s->let_cells = c.let_cells;

@@ -48,6 +48,18 @@ struct Ctx {
   DBuf<int64_t> req_off;
   int64_t let_bytes_sent = 0, let_bytes_recv = 0, let_cells = 0, let_leaves = 0;
   double ms_let = 0.0;
+  // balanced partition (cfg.partition = 1): equal-count Morton ranges cut at leaf boundaries
+  bool balanced = false;
+  int64_t nown = 0;                          // owned particles: global sorted positions [off, off + nown)
+  DBuf<uint64_t> keys_gat;                   // every rank's sorted keys, rank blocks
+  DBuf<uint32_t> gsrc, gsrc_tmp;             // global position -> gathered index
+  DBuf<int> ginv;                            // this rank's gathered block -> global position
+  DBuf<float4> red_send, red_recv;           // particle records (x, y, z, sigma), (alpha, global position)
+  DBuf<int> recv_gp;                         // owned particles in receive order: global position
+  std::vector<int64_t> red_scnt, red_rcnt;   // records sent to / received from each peer
+  DBuf<int> strad;                           // cells (level >= 2) holding a split point: partial M, all-reduced
+  int64_t nstrad = 0, redist_bytes = 0;
+  DBuf<float> ret_send, ret_recv, strad_buf;
 
   // ---- particles and tree (set_particles) ----
   int64_t n = 0;

@@ -493,6 +493,16 @@ const float2* octant_r(Ctx& c) {
   return c.r8.p;
 }
 
+// gather (dir 0: M rows of the listed cells -> packed buffer) or scatter (dir 1)
+__global__ void k_cells_copy(const int* __restrict__ ids, int64_t nid, int64_t rows, const float2* __restrict__ src,
+                             float2* __restrict__ dst, int dir) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nid * rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / rows, r = i - k * rows, cell = ids[k];
+    if (dir == 0) dst[i] = src[cell * rows + r];
+    else dst[cell * rows + r] = src[i];
+  }
+}
+
 void upward_pass(Ctx& c) {
   cudaStream_t st = c.stream;
   int P = c.P, nc = c.nc;
@@ -513,6 +523,17 @@ void upward_pass(Ctx& c) {
   }
   // root and level-1 cells (the tiles) are needed by every rank's far field
   if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc * c.level_begin[2]);
+  // balanced partition: deeper cells holding a rank boundary carry per-rank
+  // partial multipoles (their remote children are zero here) -> summed
+  if (c.balanced && c.nstrad > 0) {
+    const int64_t rows = 3 * (int64_t)nc;     // float2 per cell
+    c.strad_buf.reserve(2 * rows * c.nstrad);
+    FMM_LAUNCH(c, k_cells_copy, nblocks(rows * c.nstrad, 256), 256, 0, c.strad.p, c.nstrad, rows, (const float2*)c.M.p,
+               (float2*)c.strad_buf.p, 0);
+    allreduce_sum_f32(c, c.strad_buf.p, 2 * rows * c.nstrad);
+    FMM_LAUNCH(c, k_cells_copy, nblocks(rows * c.nstrad, 256), 256, 0, c.strad.p, c.nstrad, rows,
+               (const float2*)c.strad_buf.p, c.M.p, 1);
+  }
 }
 
 void m2l_pass(Ctx& c) {

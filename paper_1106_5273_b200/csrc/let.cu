@@ -156,10 +156,10 @@ void let_exchange(Ctx& c) {
   FMM_CUDA(cudaMemsetAsync(c.need.p, 0, sizeof(int) * nc, st));
   if (c.nm2l)
     FMM_LAUNCH(c, k_mark_remote, grid_for(c.nm2l), 256, 0, c.m2l.p, c.nm2l, 1, c.cells.begin.p, c.cells.count.p,
-               c.off, c.n, c.need.p);
+               c.off, c.nown, c.need.p);
   if (c.np2p)
     FMM_LAUNCH(c, k_mark_remote, grid_for(c.np2p), 256, 0, c.p2p.p, c.np2p, 2, c.cells.begin.p, c.cells.count.p,
-               c.off, c.n, c.need.p);
+               c.off, c.nown, c.need.p);
   // 2. compact (ascending cell id) and group by owner (stable)
   c.flags.reserve(nc);
   c.scan.reserve(nc);

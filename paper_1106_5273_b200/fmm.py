@@ -25,7 +25,8 @@ class fmm_config(C.Structure):
                 ("theta_den", C.c_int32), ("ncrit", C.c_int32), ("images", C.c_int32),
                 ("box_lo", C.c_double * 3), ("box_len", C.c_double), ("traversal", C.c_int32),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_id", C.c_void_p), ("tiles", C.c_int32 * 3), ("m2l_path", C.c_int32)]
+                ("nccl_id", C.c_void_p), ("tiles", C.c_int32 * 3), ("m2l_path", C.c_int32),
+                ("partition", C.c_int32)]
 
 
 class fmm_stats(C.Structure):
@@ -39,7 +40,8 @@ class fmm_stats(C.Structure):
                 ("ms_set_total", C.c_double), ("ms_eval_total", C.c_double),
                 ("ntot", C.c_int64), ("let_bytes_sent", C.c_int64), ("let_bytes_recv", C.c_int64),
                 ("let_cells", C.c_int64), ("let_leaves", C.c_int64), ("ms_let", C.c_double),
-                ("m2l_tc_list", C.c_int64)]
+                ("m2l_tc_list", C.c_int64), ("own_begin", C.c_int64), ("own_count", C.c_int64),
+                ("redist_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "struct_size"}

@@ -130,3 +130,25 @@ def taylor_green_octants(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
     o = ((x[:, 0] >= mid).astype(int) | ((x[:, 1] >= mid).astype(int) << 1) | ((x[:, 2] >= mid).astype(int) << 2))
     keep = (o >= 8 * rank // nranks) & (o < 8 * (rank + 1) // nranks)
     return x[keep], a[keep], s[keep]
+
+
+def clustered_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI):
+    """Non-uniform workload for the balanced partition (NEXT-3): half the
+    particles uniform in the periodic cube, half in a Gaussian cluster of
+    width L/16 (wrapped), alpha ~ N(0,1) h^3 with h = L / n^(1/3), sigma = h."""
+    rng = np.random.default_rng(seed)
+    h = L / round(n ** (1.0 / 3.0))
+    m = n // 2
+    xu = rng.uniform(lo, lo + L, size=(n - m, 3))
+    xc = lo + np.mod(0.3 * L + rng.normal(0.0, L / 16, size=(m, 3)), L)
+    x = np.concatenate([xu, xc]).astype(np.float32)
+    a = (rng.standard_normal((n, 3)) * h ** 3).astype(np.float32)
+    s = np.full(n, h, dtype=np.float32)
+    return x, a, s
+
+
+def scatter_to_ranks(n: int, nranks: int, rank: int, seed: int = 5273):
+    """Indices of the particles rank `rank` passes in the balanced-partition
+    tests: a seeded random assignment (every rank holds an arbitrary subset)."""
+    owner = np.random.default_rng(seed).integers(0, nranks, size=n)
+    return np.nonzero(owner == rank)[0]

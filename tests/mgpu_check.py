@@ -47,7 +47,7 @@ def run(fmm, x, a, s, parts=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=16)
-    ap.add_argument("--mode", choices=["tiled", "refined"], default="tiled")
+    ap.add_argument("--mode", choices=["tiled", "refined", "balanced", "balanced_cloud"], default="tiled")
     args = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -56,10 +56,18 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [P.fmm_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    gen = synth.taylor_green_tile if args.mode == "tiled" else synth.taylor_green_rank
+    balanced = args.mode.startswith("balanced")
+    if balanced:
+        # NEXT-3: every rank passes an arbitrary (seeded random) subset; the
+        # library cuts equal-count Morton ranges at leaf boundaries
+        full = synth.taylor_green(args.side) if args.mode == "balanced" else synth.clustered_cloud(args.side ** 3)
+        gen = lambda side, w, r: tuple(v[synth.scatter_to_ranks(len(full[0]), w, r)] for v in full)
+    else:
+        gen = synth.taylor_green_tile if args.mode == "tiled" else synth.taylor_green_rank
     tiles = synth.RANK_TILES[world] if args.mode == "tiled" else (1, 1, 1)
     x, a, s = gen(args.side, world, rank)
-    fmm = P.FMM(images=3, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles)
+    fmm = P.FMM(images=3, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles,
+                partition=1 if balanced else 0)
     un, sn = run(fmm, x, a, s, parts=1)
     u, st = run(fmm, x, a, s)
     p2p, m2l = P.fmm_get_lists(fmm.ctx)
@@ -80,8 +88,23 @@ def main():
         cells = P.fmm_get_cells(single.ctx)
         single.close()
         off = np.cumsum([0] + [g["n"] for g in gathered])
+        if balanced:
+            # owned ranges partition [0, N), cut at leaf boundaries; a rank's
+            # targets are the cells overlapping its range
+            ob = [(g["stats"]["own_begin"], g["stats"]["own_count"]) for g in gathered]
+            off = np.array([b for b, _ in ob] + [ob[-1][0] + ob[-1][1]])
+            leaves = cells[cells[:, 9] == 1]
+            ends = set(leaves[:, 4].tolist()) | set((leaves[:, 4] + leaves[:, 5]).tolist())
+            msg["own_ranges"] = [int(v) for v in off]
+            msg["ranges_ok"] = bool(off[0] == 0 and off[-1] == len(X) and np.all(np.diff(off) >= 0)
+                                    and all(int(v) in ends for v in off))
+            msg["imbalance"] = float(np.diff(off).max() / (len(X) / world))
+            ok &= msg["ranges_ok"]
         for r in range(world):
-            owned = (cells[:, 4] >= off[r]) & (cells[:, 4] + cells[:, 5] <= off[r + 1])
+            if balanced:
+                owned = (cells[:, 4] < off[r + 1]) & (cells[:, 4] + cells[:, 5] > off[r])
+            else:
+                owned = (cells[:, 4] >= off[r]) & (cells[:, 4] + cells[:, 5] <= off[r + 1])
             for name, glst in (("p2p", gp2p), ("m2l", gm2l)):
                 want = glst[owned[glst[:, 0]]]
                 got = gathered[r][name]
@@ -98,12 +121,13 @@ def main():
         msg["full_vs_single_u"] = rel(DU, U)
         msg["full_vs_single_s"] = rel(DS, SS)
         ok &= msg["full_vs_single_u"] <= 1e-6 and msg["full_vs_single_s"] <= 1e-6
-        uc, sc = tg_closed(X, A, S[0])
-        msg["closed_form_u"] = rel(DU, uc)
-        msg["closed_form_s"] = rel(DS, sc)
-        ok &= msg["closed_form_u"] <= 1e-3 and msg["closed_form_s"] <= 1e-3
+        if args.mode != "balanced_cloud":
+            uc, sc = tg_closed(X, A, S[0])
+            msg["closed_form_u"] = rel(DU, uc)
+            msg["closed_form_s"] = rel(DS, sc)
+            ok &= msg["closed_form_u"] <= 1e-3 and msg["closed_form_s"] <= 1e-3
         msg["let"] = [{k: g["stats"][k] for k in ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves",
-                                                   "ms_let")} for g in gathered]
+                                                   "ms_let", "redist_bytes")} for g in gathered]
         msg["ok"] = bool(ok)
         msg["world"] = world
         msg["mode"] = args.mode

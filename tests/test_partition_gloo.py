@@ -89,3 +89,87 @@ def test_two_rank_let_requests_gloo():
         p.join(timeout=60)
     assert all(r[1] for r in res), res
     assert all(r[2] + r[3] > 0 for r in res), res      # a real exchange happens
+
+
+def _balanced_worker(rank, world, port, q):
+    """Model of the balanced partition (cfg.partition = 1, NEXT-3):
+    every rank holds a random subset of a clustered cloud; the Morton curve of
+    the global tree is cut into equal-count ranges moved to the nearest leaf
+    boundary (the library's k_splits rule), particles are sent to their owners
+    (counts exchanged with gloo) and straddling cells are the only partial
+    multipoles."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        x, a, s = synth.clustered_cloud(3000)
+        mine = synth.scatter_to_ranks(len(x), world, rank)
+        f = oracle.OracleFMM(x, a, s, images=1, ncrit=16)
+        cells = f.cells()
+        _keys, perm = f.keys()                  # perm[g] = input index at global position g
+        N = len(x)
+        b0, cnt, leaf = cells[:, 4], cells[:, 5], cells[:, 9]
+        cb, nch = cells[:, 7], cells[:, 8]
+
+        def split(k):                           # the leaf holding k N / P, nearer boundary
+            xk = k * N // world
+            c = 0
+            while not leaf[c]:
+                kids = range(cb[c], cb[c] + nch[c])
+                c = next((ch for ch in kids if xk < b0[ch] + cnt[ch]), cb[c] + nch[c] - 1)
+            return b0[c] if xk - b0[c] <= b0[c] + cnt[c] - xk else b0[c] + cnt[c]
+
+        off = np.array([0] + [split(k) for k in range(1, world)] + [N])
+        ok = bool(np.all(np.diff(off) >= 0))
+        # no leaf is cut
+        lv = np.nonzero(leaf)[0]
+        for k in range(1, world):
+            ok &= not bool(np.any((b0[lv] < off[k]) & (off[k] < b0[lv] + cnt[lv])))
+        # balance: every range within one leaf of N / P
+        ok &= bool(np.all(np.abs(np.diff(off) - N / world) <= 2 * 16 + 1))
+        # redistribution counts: my particles' global positions -> owners
+        gpos = np.empty(N, dtype=np.int64)
+        gpos[perm] = np.arange(N)
+        owner = np.searchsorted(off, gpos[mine], side="right") - 1
+        send = torch.tensor(np.bincount(owner, minlength=world), dtype=torch.int64)
+        recv = torch.zeros(world, dtype=torch.int64)
+        dist.all_to_all_single(recv, send)
+        ok &= int(recv.sum()) == int(off[rank + 1] - off[rank])
+        # straddling cells: non-leaves only, nested (at most one per level per split)
+        st = np.zeros(len(cells), dtype=bool)
+        for k in range(1, world):
+            st |= (b0 < off[k]) & (off[k] < b0 + cnt)
+        ok &= not bool(np.any(st & (leaf == 1)))
+        lev = cells[:, 0]
+        for k in range(1, world):
+            sk = (b0 < off[k]) & (off[k] < b0 + cnt)
+            ok &= bool(np.all(np.bincount(lev[sk]) <= 1))
+        # M is linear: the per-rank partial multipoles of a straddling cell
+        # (its particles split by owner) sum to the full one -- modelled on the
+        # monopole (sum of alpha) of every straddling cell
+        for c in np.nonzero(st)[0]:
+            idx = perm[b0[c]:b0[c] + cnt[c]]
+            gp = np.arange(b0[c], b0[c] + cnt[c])
+            mono = torch.tensor(a[idx[(gp >= off[rank]) & (gp < off[rank + 1])]].astype(np.float64).sum(0))
+            dist.all_reduce(mono)
+            ok &= bool(np.allclose(mono.numpy(), a[idx].astype(np.float64).sum(0), rtol=1e-12, atol=1e-18))
+        q.put((rank, bool(ok), int(st.sum()), [int(v) for v in off]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_rank_balanced_partition_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    port = 29660
+    procs = [ctx.Process(target=_balanced_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] for r in res), res
+    assert all(r[2] > 0 for r in res), res              # the splits cut through some cells
+    assert len({tuple(r[3]) for r in res}) == 1, res    # all ranks agree on the ranges
