@@ -57,6 +57,10 @@ def parse():
                     help="N > 1: tiled = C5 weak scaling (one 2pi tile of side^3 per GPU, reading Z27); "
                          "refined = the fixed box refined to side*(1..2) per axis; "
                          "strong = C4: one side^3 lattice split over the GPUs by Morton octants")
+    ap.add_argument("--partition", choices=["octant", "balanced"], default="octant",
+                    help="N > 1 with --mode strong: octant = each rank passes its Morton-octant block; balanced = "
+                         "each rank passes a random 1/N subset and the library redistributes it every step "
+                         "(cfg.partition = 1: equal-count Morton ranges cut at leaf boundaries, NEXT-3)")
     ap.add_argument("--cpu-sample", type=int, default=32, help="oracle sample: TG n^3 lattice")
     ap.add_argument("--ref-sample", type=int, default=24, help="--impl reference sample: TG n^3 lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -215,7 +219,14 @@ def main():
     tiles = synth.RANK_TILES[world] if tiled else (1, 1, 1)
     gen = {"tiled": synth.taylor_green_tile, "refined": synth.taylor_green_rank,
            "strong": synth.taylor_green_octants}[args.mode]
-    x, a, s = gen(args.side, world, rank)
+    balanced = world > 1 and args.partition == "balanced"
+    if balanced and args.mode != "strong":
+        raise SystemExit("--partition balanced needs --mode strong")
+    if balanced:
+        full = synth.taylor_green(args.side)
+        x, a, s = (v[synth.scatter_to_ranks(len(full[0]), world, rank)] for v in full)
+    else:
+        x, a, s = gen(args.side, world, rank)
     n = len(x)
     stream = torch.cuda.Stream()
     nccl_id = None
@@ -224,7 +235,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     f = P.FMM(order=args.order, images=args.images, theta=theta, ncrit=args.ncrit, device=local,
-              stream=stream.cuda_stream, nranks=world, rank=rank, nccl_id=nccl_id, tiles=tiles)
+              stream=stream.cuda_stream, nranks=world, rank=rank, nccl_id=nccl_id, tiles=tiles,
+              partition=1 if balanced else 0)
     with torch.cuda.stream(stream):
         xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
         ud = torch.empty((n, 3), device="cuda")
@@ -363,16 +375,20 @@ def main():
                         "periodic k=%d, p=%d, theta=%s, ncrit=%d" %
                         ("x".join(str(args.side * m) for m in synth.RANK_LATTICE[world]), n,
                          args.images, args.order, args.theta, args.ncrit)) if args.mode == "refined" else
-                       ("C4 strong scaling: Taylor-Green %d^3 in [-pi,pi)^3 split by Morton octants, %d particles on "
+                       ("C4 strong scaling: Taylor-Green %d^3 in [-pi,pi)^3 %s, %d particles on "
                         "this GPU, periodic k=%d, p=%d, theta=%s, ncrit=%d" %
-                        (args.side, n, args.images, args.order, args.theta, args.ncrit)),
+                        (args.side, "passed as random 1/N subsets and redistributed by the library every step "
+                         "(balanced partition: equal-count Morton ranges cut at leaf boundaries)" if balanced else
+                         "split by Morton octants", n, args.images, args.order, args.theta, args.ncrit)),
                        "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
                        "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),
                        "parallelism": "1 GPU" if world == 1 else
-                       "%d GPUs: Morton-octant domain decomposition, exact LET (multipoles + bodies) over "
-                       "NCCL grouped send/recv, root multipole all-reduce" % world},
+                       "%d GPUs: %s domain decomposition, exact LET (multipoles + bodies) over "
+                       "NCCL grouped send/recv, root multipole all-reduce" %
+                       (world, "balanced Morton-range (partition = 1)" if balanced else "Morton-octant")},
             "let": None if world == 1 else {k: statistics.mean(st[k] for st in stats) for k in
-                                            ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves", "ms_let")},
+                                            ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves", "ms_let",
+                                             "redist_bytes")},
             "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
             "particles_per_s": tot_n / (ms_max * 1e-3),
             "phases_ms": phase,
