@@ -299,3 +299,50 @@ def rk2_step(x, alpha, sigma, dt, nu=0.0, images=0, box_len=2 * np.pi):
     sh = np.sqrt(sigma ** 2 + nu * dt)
     u2, s2 = direct(xh, ah, xh, ah, sh, box_len, images)
     return x + dt * u2, alpha + dt * s2, np.sqrt(sigma ** 2 + 2 * nu * dt)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: RBF reinitialisation -- plain numpy, double precision.
+# zeta is the Gaussian core whose radial mass is g(rho) of Eq. 2;
+# b_i = sum_j alpha_j zeta_{sigma_j}(y_i - x_j) is the old field's vorticity at
+# the sites, and beta solves the collocation system sum_k beta_k
+# zeta_{sigma0}(y_i - y_k) = b_i (Gaussian basis = the RBF).  The oracle forms
+# the dense matrix and solves it exactly (LAPACK); sums run over the first
+# image layer (27 boxes) when periodic, as the GPU's P2P lists do (reading R1).
+# Pinned by tests/test_oracle_rbf.py.
+# --------------------------------------------------------------------------
+def zeta(r2, s):
+    """(2 pi s^2)^{-3/2} exp(-r^2 / (2 s^2)) -- the vorticity of a unit blob."""
+    s = np.asarray(s, dtype=np.float64)
+    return np.exp(-np.asarray(r2, dtype=np.float64) / (2.0 * s * s)) / (2.0 * np.pi * s * s) ** 1.5
+
+
+def _shifts(images, box_len):
+    if images == 0:
+        return np.zeros((1, 3))
+    g = np.arange(-1, 2) * box_len
+    return np.array([[a, b, c] for c in g for b in g for a in g], dtype=np.float64)
+
+
+def gauss_field(y, x, alpha, sigma, box_len=2 * np.pi, images=1):
+    """b[i] = sum over the image shifts and j of alpha_j zeta_{sigma_j}(y_i - x_j - shift)."""
+    y = np.asarray(y, np.float64)
+    x = np.asarray(x, np.float64)
+    alpha = np.asarray(alpha, np.float64)
+    sigma = np.asarray(sigma, np.float64)
+    out = np.zeros((len(y), 3))
+    for sh in _shifts(images, box_len):
+        d = y[:, None, :] - x[None, :, :] - sh
+        out += zeta((d * d).sum(-1), sigma[None, :]) @ alpha
+    return out
+
+
+def rbf_reinit(x, alpha, sigma, y, sigma0, box_len=2 * np.pi, images=1):
+    """beta[m][3] solving sum_k beta_k zeta_{sigma0}(y_i - y_k) = b_i exactly."""
+    y = np.asarray(y, np.float64)
+    b = gauss_field(y, x, alpha, sigma, box_len, images)
+    A = np.zeros((len(y), len(y)))
+    for sh in _shifts(images, box_len):
+        d = y[:, None, :] - y[None, :, :] - sh
+        A += zeta((d * d).sum(-1), sigma0)
+    return np.linalg.solve(A, b)
