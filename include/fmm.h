@@ -56,7 +56,9 @@ typedef enum {
   FMM_E_OOM = 5,        /* device allocation failed                            */
   FMM_E_CUDA = 6,       /* CUDA runtime error (context poisoned)               */
   FMM_E_NCCL = 7,       /* NCCL error (context poisoned)                       */
-  FMM_E_INTERNAL = 8    /* invariant violated (context poisoned)               */
+  FMM_E_INTERNAL = 8,   /* invariant violated (context poisoned)               */
+  FMM_E_NOCONV = 9      /* fmm_rbf_reinit: CG reached maxit above tol; the
+                           outputs hold the last iterate and its residual       */
 } fmm_status;
 
 typedef struct {
@@ -189,6 +191,28 @@ fmm_status fmm_step(fmm_ctx* ctx, int64_t n, float* x, float* alpha, float* sigm
  * Single-GPU in this build.  Errors: as fmm_set_particles / fmm_evaluate. */
 fmm_status fmm_evaluate_targets(fmm_ctx* ctx, int64_t n, const float* x, const float* alpha,
                                 const float* sigma, int64_t nt, const float* y, float* u);
+
+/* NEXT-4: radial-basis-function reinitialisation of the particle
+ * field onto m new sites ("radial basis function interpolation for
+ * reinitialized Gaussian distributions"; the sites are the same every
+ * time, so their tree is reused).  With the Gaussian core of Eq. 2,
+ * zeta_s(r) = (2 pi s^2)^(-3/2) exp(-r^2 / (2 s^2)), the old field's vorticity at
+ * site i is b_i = sum_j alpha_j zeta_{sigma_j}(y_i - x_j) (periodic images as the
+ * config's first layer) and the new strengths beta[m][3] (core sigma0 on every
+ * site) solve sum_k beta_k zeta_{sigma0}(y_i - y_k) = b_i by conjugate gradients
+ * (A is symmetric positive definite) to ||b - A beta|| <= tol ||b||, at most
+ * maxit iterations.  Both sums run over the P2P lists of the tree (DESIGN.md
+ * reading R1).  Inputs x[n][3], alpha[n][3], sigma[n], y[m][3]; output
+ * beta[m][3] in the order of y (overwrite); pointers host or device.  *iters
+ * and *resid (may be NULL) receive the iteration count and the final relative
+ * residual.  Afterwards the context holds the sites with strengths beta and
+ * core sigma0 (evaluate may follow).  Single GPU in this build.  Errors:
+ * FMM_E_ARG (bad arguments, nranks > 1, sigma0 <= 0, tol <= 0, maxit < 1),
+ * FMM_E_NOCONV (maxit reached above tol; outputs hold the last iterate), and
+ * those of set_particles. */
+fmm_status fmm_rbf_reinit(fmm_ctx* ctx, int64_t n, const float* x, const float* alpha, const float* sigma,
+                          int64_t m, const float* y, float sigma0, double tol, int32_t maxit, float* beta,
+                          int32_t* iters, double* resid);
 
 /* Multi-GPU bootstrap: writes a fresh 128-byte ncclUniqueId into id (one rank
  * calls it and broadcasts the bytes to the others, e.g. via torch.distributed;

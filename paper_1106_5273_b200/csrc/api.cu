@@ -556,6 +556,32 @@ FMM_API fmm_status fmm_step(fmm_ctx* h, int64_t n, float* x, float* alpha, float
   });
 }
 
+FMM_API fmm_status fmm_rbf_reinit(fmm_ctx* h, int64_t n, const float* x, const float* alpha, const float* sigma,
+                                  int64_t m, const float* y, float sigma0, double tol, int32_t maxit, float* beta,
+                                  int32_t* iters, double* resid) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  int it = 0;
+  double res = 0.0;
+  fmm_status st = guard(&c, [&] {
+    if (n < 0 || m < 1 || (n > 0 && (!x || !alpha || !sigma)) || !y || !beta)
+      throw FmmError(FMM_E_ARG, "bad arguments");
+    if (!(sigma0 > 0.0f) || !std::isfinite(sigma0)) throw FmmError(FMM_E_SIGMA, "sigma0 must be > 0");
+    if (!(tol > 0.0) || maxit < 1) throw FmmError(FMM_E_ARG, "tol must be > 0 and maxit >= 1");
+    if (c.cfg.nranks > 1) throw FmmError(FMM_E_ARG, "fmm_rbf_reinit is single-GPU in this build");
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    rbf_reinit_impl(c, n, x, alpha, sigma, m, y, sigma0, tol, (int)maxit, beta, &it, &res);
+  });
+  if (iters) *iters = it;
+  if (resid) *resid = res;
+  if (st == FMM_OK && res > tol) {
+    c.err = "fmm_rbf_reinit: no convergence in maxit iterations (relative residual above tol)";
+    return FMM_E_NOCONV;
+  }
+  return st;
+}
+
 FMM_API fmm_status fmm_evaluate_targets(fmm_ctx* h, int64_t n, const float* x, const float* alpha, const float* sigma,
                                         int64_t nt, const float* y, float* u) {
   if (!h) return FMM_E_ARG;

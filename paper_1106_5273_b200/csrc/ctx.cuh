@@ -117,6 +117,10 @@ struct Ctx {
   // ---- time step (NEXT-1) ----
   DBuf<float> st_x, st_a, st_s, st_u, st_da, st_xh, st_ah, st_sh;
 
+  // ---- RBF reinitialisation (NEXT-4) ----
+  DBuf<double> rbf_b, rbf_v, rbf_x, rbf_r, rbf_p, rbf_ap, rbf_dot;
+  DBuf<float4> rbf_q;
+
   // ---- timing ----
   cudaEvent_t ev[PH_N + 1] = {};
   cudaEvent_t ev_fork = nullptr, ev_trav = nullptr;   // upward-pass / traversal overlap
@@ -152,6 +156,9 @@ void fill_f32(Ctx& c, float* p, int64_t n, float v);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g);
+void gauss_pass(Ctx& c, const float4* q, double* out);
+void rbf_reinit_impl(Ctx& c, int64_t n, const float* x, const float* alpha, const float* sigma, int64_t m,
+                     const float* y, float sigma0, double tol, int maxit, float* beta_out, int* iters, double* resid);
 
 }  // namespace fmmb
 

@@ -15,9 +15,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FMM_LIB") or os.path.join(_HERE, "libfmm_b200.so")   # FMM_LIB: development variants (tools/build_variant.py)
 
-FMM_OK, FMM_E_ARG, FMM_E_NONFINITE, FMM_E_SIGMA, FMM_E_STATE, FMM_E_OOM, FMM_E_CUDA, FMM_E_NCCL, FMM_E_INTERNAL = range(9)
+(FMM_OK, FMM_E_ARG, FMM_E_NONFINITE, FMM_E_SIGMA, FMM_E_STATE, FMM_E_OOM, FMM_E_CUDA, FMM_E_NCCL, FMM_E_INTERNAL,
+ FMM_E_NOCONV) = range(10)
 STATUS_NAMES = ["FMM_OK", "FMM_E_ARG", "FMM_E_NONFINITE", "FMM_E_SIGMA", "FMM_E_STATE", "FMM_E_OOM",
-                "FMM_E_CUDA", "FMM_E_NCCL", "FMM_E_INTERNAL"]
+                "FMM_E_CUDA", "FMM_E_NCCL", "FMM_E_INTERNAL", "FMM_E_NOCONV"]
 
 
 class fmm_config(C.Structure):
@@ -49,7 +50,7 @@ class fmm_stats(C.Structure):
 
 class FMMError(RuntimeError):
     def __init__(self, status, msg):
-        super().__init__("%s: %s" % (STATUS_NAMES[status] if 0 <= status < 9 else status, msg))
+        super().__init__("%s: %s" % (STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status, msg))
         self.status = status
 
 
@@ -83,10 +84,12 @@ def lib():
         L.fmm_comm_unique_id.argtypes = [vp]
         L.fmm_step.argtypes = [vp, i64, vp, vp, vp, C.c_double, C.c_double]
         L.fmm_evaluate_targets.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
+        L.fmm_rbf_reinit.argtypes = [vp, i64, vp, vp, vp, i64, vp, C.c_float, C.c_double, C.c_int32, vp,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
                    "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id", "fmm_step",
-                   "fmm_evaluate_targets"):
+                   "fmm_evaluate_targets", "fmm_rbf_reinit"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
@@ -217,6 +220,17 @@ def fmm_evaluate_targets(ctx, n, x, alpha, sigma, nt, y, u):
                                            _ptr(u)))
 
 
+def fmm_rbf_reinit(ctx, n, x, alpha, sigma, m, y, sigma0, tol, maxit, beta):
+    """NEXT-4: returns (iterations, relative residual); FMMError(FMM_E_NOCONV) if maxit is reached."""
+    it, res = C.c_int32(0), C.c_double(0.0)
+    st = lib().fmm_rbf_reinit(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), int(m), _ptr(y), float(sigma0),
+                              float(tol), int(maxit), _ptr(beta), C.byref(it), C.byref(res))
+    if st == FMM_E_NOCONV:
+        raise FMMError(st, "%d iterations, relative residual %.3e > tol %.1e" % (it.value, res.value, tol))
+    _check(ctx, st)
+    return it.value, res.value
+
+
 def fmm_comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     st = lib().fmm_comm_unique_id(buf)
@@ -258,6 +272,13 @@ class FMM:
         """Velocity at strength-free targets y (NEXT-2); the context then holds the union."""
         fmm_evaluate_targets(self.ctx, x.shape[0], x, alpha, sigma, y.shape[0], y, u)
         self.n = int(x.shape[0] + y.shape[0])
+
+    def rbf_reinit(self, x, alpha, sigma, y, sigma0, beta, tol=1e-6, maxit=200):
+        """RBF reinitialisation onto the sites y (NEXT-4); writes beta, returns (iters, resid).
+        The context then holds (y, beta, sigma0)."""
+        r = fmm_rbf_reinit(self.ctx, x.shape[0], x, alpha, sigma, y.shape[0], y, sigma0, tol, maxit, beta)
+        self.n = int(y.shape[0])
+        return r
 
     def stats(self):
         return fmm_get_stats(self.ctx)
