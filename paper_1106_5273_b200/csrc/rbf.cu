@@ -61,6 +61,22 @@ __global__ void __launch_bounds__(NT) k_gauss(const int* __restrict__ leaf_ids, 
       xt[h][1] = (float)((double)p.y - cy);
       xt[h][2] = (float)((double)p.z - cz);
     }
+    // tight box of this pass's targets: sources farther than 6 sigma_j from it
+    // add below e^{-18} of a peak term (under the FP32 resolution of the sums)
+    // and are not staged
+    float bcen[3], bhw[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const bool v0 = t0 + lane < tcnt, v1 = t0 + lane + NT < tcnt;
+      float lo = fminf(v0 ? xt[0][d] : 1e30f, v1 ? xt[1][d] : 1e30f);
+      float hi = fmaxf(v0 ? xt[0][d] : -1e30f, v1 ? xt[1][d] : -1e30f);
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      bcen[d] = 0.5f * (lo + hi);
+      bhw[d] = 0.5f * (hi - lo) * 1.0001f;
+    }
     for (int e = eb; e < ee; ++e) {
       const uint64_t ent = lst[e];
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
@@ -69,21 +85,36 @@ __global__ void __launch_bounds__(NT) k_gauss(const int* __restrict__ leaf_ids, 
       const int sb = c.begin[src], scnt = c.count[src];
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
+        float4 vx[2], vq[2];
+        bool keep[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int j = s0 + lane + h * NT;
+          keep[h] = false;
           if (j < scnt) {
             const float4 p = pos[sb + j];
             const float4 a = q[sb + j];
             const float w = 1.0f / (2.0f * p.w * p.w);
             const float k = (float)(1.0 / (2.0 * kPi * sqrt(2.0 * kPi))) / (p.w * p.w * p.w);   // (2 pi)^{-3/2} / s^3
-            sx[lane + h * NT] = make_float4((float)((double)p.x + sh0), (float)((double)p.y + sh1),
-                                            (float)((double)p.z + sh2), -1.4426950408889634f * w);
-            sq[lane + h * NT] = make_float4(a.x * k, a.y * k, a.z * k, 0.f);
+            vx[h] = make_float4((float)((double)p.x + sh0), (float)((double)p.y + sh1), (float)((double)p.z + sh2),
+                                -1.4426950408889634f * w);
+            vq[h] = make_float4(a.x * k, a.y * k, a.z * k, 0.f);
+            const float gx = fmaxf(0.f, fabsf(vx[h].x - bcen[0]) - bhw[0]), gy = fmaxf(0.f, fabsf(vx[h].y - bcen[1]) - bhw[1]),
+                        gz = fmaxf(0.f, fabsf(vx[h].z - bcen[2]) - bhw[2]);
+            keep[h] = (gx * gx + gy * gy + gz * gz) * w < 18.0f;
           }
         }
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned k0 = __ballot_sync(0xffffffffu, keep[0]), k1 = __ballot_sync(0xffffffffu, keep[1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!keep[h]) continue;
+          const int dst = h == 0 ? __popc(k0 & lt) : __popc(k0) + __popc(k1 & lt);
+          sx[dst] = vx[h];
+          sq[dst] = vq[h];
+        }
         __syncwarp();
-        const int nj = min(TP, scnt - s0);
+        const int nj = __popc(k0) + __popc(k1);
         float part[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
         for (int jj = 0; jj < nj; ++jj) {
           const float4 v = sx[jj], a = sq[jj];
