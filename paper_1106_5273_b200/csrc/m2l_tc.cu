@@ -73,15 +73,23 @@ namespace {
 #endif
 constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
 constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
-constexpr int kRows = 256;                  // rows (target, component) per CTA
+#ifndef TC_ROWS
+#define TC_ROWS 256
+#endif
+#ifndef TC_STAGES
+#define TC_STAGES 4
+#endif
+constexpr int kRows = TC_ROWS;              // rows (target, component) per CTA: 128 x kAcc
+constexpr int kAcc = kRows / 128;           // TMEM accumulators per CTA
+constexpr int kCtasPerSm = 512 / kRows;     // 2 (256 rows) or 4 (128 rows) CTAs per SM
 constexpr int kN = 112;                     // local-expansion reals (110, padded)
 constexpr int kKB = 8;                      // K per stage (one kind::tf32 MMA)
 constexpr int kNKB = 14;                    // K-blocks per offset (112 / 8)
-constexpr int kStages = 4;
+constexpr int kStages = TC_STAGES;
 constexpr int kPF = TC_PF;                      // gather prefetch distance (stages)
 constexpr int kATile = 128 * kKB * 4;       // one 128-row A tile (hi or lo), bytes
 constexpr int kALbo = 16 * 128;             // A tile: stride between its two 16-byte K chunks
-constexpr int kAStage = 2 * 2 * kATile;     // 2 accumulators x (hi, lo)
+constexpr int kAStage = kAcc * 2 * kATile;  // accumulators x (hi, lo)
 constexpr int kBMax = 2 * kN * kKB * 4;     // operator slice (hi + lo) at N = 112
 constexpr int kStage = kAStage + kBMax;
 constexpr int kThreads = kRows + 32;
@@ -448,7 +456,7 @@ struct TcArgs {
   int nlv;
 };
 
-__global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T, TcGeo g,
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, TcTables T, TcGeo g,
                                                         const float4* __restrict__ Mp, float2* __restrict__ Lc) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full[kStages], empty[kStages], chunk_full, drained[2];
@@ -462,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
   const int nchunk = (nit + CN - 1) / CN;
 
   if (warp == kRows / 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(saddr(&tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tbase)), "n"(kAcc * 128));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
       const uint64_t bh = umma_desc(st + kAStage, nc / 8 * 128);
       const uint64_t bl = umma_desc(st + kAStage + nc * kKB * 4, nc / 8 * 128);
 #pragma unroll
-      for (int tau = 0; tau < 2; ++tau) {
+      for (int tau = 0; tau < kAcc; ++tau) {
         const uint64_t ah = umma_desc(st + (tau * 2 + 0) * kATile, 16 * 128);
         const uint64_t al = umma_desc(st + (tau * 2 + 1) * kATile, 16 * 128);
         const uint32_t dt = tmem + (uint32_t)(tau * 128);
@@ -632,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_m2l_tc(TcArgs args, TcTables T,
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 128));
 }
 
 TcGeo make_geo(Ctx& c) {
