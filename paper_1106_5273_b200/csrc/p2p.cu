@@ -395,12 +395,12 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   c.dnear.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
-  // 16 blocks/SM (128 registers), far loop unrolled 4x, near 2x: the best of
-  // the occupancy/unroll sweep on C3 (tools/p2p_sweep.py history)
+  // 16 blocks/SM (128 registers), far loop unrolled 4x, near 4x: the best of
+  // the occupancy/unroll sweep on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8, <12,4,2> 210.2)
   c.posl.reserve(std::max<int64_t>(c.ntot, 1));
   FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
              (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p);
-  FMM_LAUNCH(c, (k_p2p<16, 4, 2>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
+  FMM_LAUNCH(c, (k_p2p<16, 4, 4>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
              c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
              c.dnear.p);
 }
