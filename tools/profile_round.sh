@@ -22,4 +22,12 @@ cp profiles/latest_p2p.json $OUT/latest_p2p.json
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $B > /dev/null 2>&1
 python tools/ncu_summary.py $OUT/launches.csv > $OUT/launches_summary.json 2>&1
+# every kernel of one step with DRAM bytes, FMA / issue / tensor utilisation (HBM GB/s of keys, sort, tree)
+K="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"
+K=$K,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed
+timeout 900 ncu --metrics $K --clock-control none --csv --log-file $OUT/all_kernels.csv $B > /dev/null 2>&1
+python tools/ncu_summary.py $OUT/all_kernels.csv $OUT/all_kernels.json > $OUT/all_kernels.txt 2>&1
+# the tensor-core M2L, full set
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_m2l_tc -c 1 -o $OUT/m2l_tc $B > /dev/null 2>&1
+ncu -i $OUT/m2l_tc.ncu-rep --page raw --csv > $OUT/m2l_tc_raw.csv 2>/dev/null
 echo done
