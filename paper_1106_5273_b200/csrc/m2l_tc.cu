@@ -34,14 +34,14 @@
 // oracle (tests/test_gpu_m2l_tc.py).
 //
 // Pipeline (two CTAs per SM, 9 warps each): rows are (target, component),
-// 256 per CTA as two 128-row accumulators in TMEM.  Warps 0-7 gather the 8
-// multipole reals of the current K-block for every row from a 16-byte-aligned
-// packed copy of M (two threads per row, one 16-byte chunk each), apply the
-// row's S_M signs, split hi/lo and store the stage's A tiles (K-major
-// core-matrix layout, no swizzle); thread 0 also bulk-copies the stage's
-// pre-split operator slice (cp.async.bulk, mbarrier tx count).  One thread of
-// warp 8 issues the 6 MMAs of a stage and commits to the stage's "empty"
-// mbarrier.  Targets are processed in Morton order so concurrently running
+// 256 per CTA as two 128-row accumulators in TMEM.  A stage is TC_KPS = 2
+// K-blocks of one offset.  Warps 0-7 gather, for every row, the 2 x 8
+// multipole reals of the stage from a packed copy of M (one thread per row,
+// one 256-bit load per K-block), apply the row's S_M signs, split hi/lo and
+// store the stage's A tiles (K-major core-matrix layout, no swizzle); thread 0
+// also bulk-copies the stage's pre-split operator slices (cp.async.bulk,
+// mbarrier tx count).  One thread of warp 8 issues the 12 MMAs of a stage and
+// commits to the stage's "empty" mbarrier.  Targets are processed in Morton order so concurrently running
 // CTAs share their sources in L2.
 //
 // Which cells take this path is decided per list build: a reference cell
@@ -66,7 +66,7 @@ namespace {
 #define TC_CHUNK 32
 #endif
 #ifndef TC_PF
-#define TC_PF 6
+#define TC_PF (TC_KPS == 1 ? 6 : 3)
 #endif
 #ifndef TC_DIAG
 #define TC_DIAG 0   // development only (tools/build_variant.py): 1 = every row reads its own cell, 2 = no gathers
@@ -76,8 +76,14 @@ constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
 #ifndef TC_ROWS
 #define TC_ROWS 256
 #endif
+#ifndef TC_KPS
+#define TC_KPS 2                 // K-blocks per pipeline stage (1 or 2): each stage hand-off (256
+                                 // producer arrivals, proxy fences, the MMA issuer's wait, the
+                                 // commit) bounds the kernel, so two K-blocks per stage halve the
+                                 // hand-offs: C3 M2L phase 68.9 -> 54.4 ms (2 stages of 46 KB)
+#endif
 #ifndef TC_STAGES
-#define TC_STAGES 4
+#define TC_STAGES (TC_KPS == 1 ? 4 : 2)
 #endif
 constexpr int kRows = TC_ROWS;              // rows (target, component) per CTA: 128 x kAcc
 constexpr int kAcc = kRows / 128;           // TMEM accumulators per CTA
@@ -89,8 +95,10 @@ constexpr int kStages = TC_STAGES;
 constexpr int kPF = TC_PF;                      // gather prefetch distance (stages)
 constexpr int kATile = 128 * kKB * 4;       // one 128-row A tile (hi or lo), bytes
 constexpr int kALbo = 16 * 128;             // A tile: stride between its two 16-byte K chunks
-constexpr int kAStage = kAcc * 2 * kATile;  // accumulators x (hi, lo)
-constexpr int kBMax = 2 * kN * kKB * 4;     // operator slice (hi + lo) at N = 112
+constexpr int kKPS = TC_KPS;
+constexpr int kSPO = kNKB / kKPS;            // stages per offset
+constexpr int kAStage = kKPS * kAcc * 2 * kATile;  // K-blocks x accumulators x (hi, lo)
+constexpr int kBMax = kKPS * 2 * kN * kKB * 4;   // operator slices (hi + lo) at N <= 112
 constexpr int kStage = kAStage + kBMax;
 constexpr int kThreads = kRows + 32;
 // offsets accumulated in TMEM between drains: each drain stalls the CTA's MMAs
@@ -465,8 +473,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   int li = 0;
   while (li + 1 < args.nlv && (int)blockIdx.x >= args.lv[li + 1].cta_begin) ++li;
   const TcLevelArg A = args.lv[li];
-  const int nit = A.D * kNKB;
-  constexpr int CN = kChunk * kNKB;
+  const int nit = A.D * kSPO;                   // pipeline stages
+  constexpr int CN = kChunk * kSPO;
   const int nchunk = (nit + CN - 1) / CN;
 
   if (warp == kRows / 32) {
@@ -508,8 +516,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
       ct[2] = (2 * g.qz[cell] + 1) << (kMaxLevel - A.lt);
     }
     int pf_d = -1;
-    auto load = [&](int it, float (&v)[8]) {
-      const int d = it / kNKB, kb = it - kNKB * (it / kNKB);
+    auto load = [&](int it, float (&v)[8 * kKPS]) {
+      const int d = it / kSPO, kb = (it - kSPO * (it / kSPO)) * kKPS;
       if (d != pf_d) {
         pf_d = d;
         const int code = __ldg(A.codes + d);
@@ -521,12 +529,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
         src = (const float*)Mp + ((size_t)s * kNKB * kMpLine + comp * 2) * 4;
       }
 #if TC_DIAG == 2
-      for (int q = 0; q < 8; ++q) v[q] = __int_as_float(kb + q);   // diagnostic: no loads
+      for (int q = 0; q < 8 * kKPS; ++q) v[q] = __int_as_float(kb + q);   // diagnostic: no loads
       return;
 #endif
-      asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                   : "l"(src + kb * kMpLine * 4));
+#pragma unroll
+      for (int b = 0; b < kKPS; ++b)
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(v[8 * b + 0]), "=f"(v[8 * b + 1]), "=f"(v[8 * b + 2]), "=f"(v[8 * b + 3]),
+                       "=f"(v[8 * b + 4]), "=f"(v[8 * b + 5]), "=f"(v[8 * b + 6]), "=f"(v[8 * b + 7])
+                     : "l"(src + (kb + b) * kMpLine * 4));
     };
     // drains: thread tid owns row tid (TMEM lane quarter = warp % 4); the
     // chunk's sums are added into Lc with vector reductions (REDG.ADD.F32x2:
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
     };
     const int rr = tid & 127, tau = tid >> 7;
     const int arow = (rr >> 3) * 128 + (rr & 7) * 16;
-    float buf[kPF][8];
+    float buf[kPF][8 * kKPS];
 #pragma unroll
     for (int u = 0; u < kPF; ++u)
       if (u < nit) load(u, buf[u]);
@@ -578,27 +589,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
         if (it < nit) {
           if (it >= CN && it % CN == 0) drain();         // chunk it/CN - 1 is complete
           const int s = it % kStages;
-          const int kb = it - kNKB * (it / kNKB);
+          const int kb0 = (it - kSPO * (it / kSPO)) * kKPS;
           if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
           unsigned char* st = smem + (size_t)s * kStage;
-          const uint32_t sg = (uint32_t)T.sm[cls][kb];              // S_M of the row's class
-          float hi[8], lo[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float x = __uint_as_float(__float_as_uint(buf[u][q]) ^ (((sg >> q) & 1u) << 31));
-            hi[q] = tf32_hi(x);
-            lo[q] = x - hi[q];
+          for (int b = 0; b < kKPS; ++b) {
+            const uint32_t sg = (uint32_t)T.sm[cls][kb0 + b];         // S_M of the row's class
+            float hi[8], lo[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float x = __uint_as_float(__float_as_uint(buf[u][8 * b + q]) ^ (((sg >> q) & 1u) << 31));
+              hi[q] = tf32_hi(x);
+              lo[q] = x - hi[q];
+            }
+            unsigned char* ah = st + ((b * kAcc + tau) * 2 + 0) * kATile + arow;
+            unsigned char* al = st + ((b * kAcc + tau) * 2 + 1) * kATile + arow;
+            *(float4*)ah = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *(float4*)(ah + kALbo) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+            *(float4*)al = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            *(float4*)(al + kALbo) = make_float4(lo[4], lo[5], lo[6], lo[7]);
           }
-          unsigned char* ah = st + (tau * 2 + 0) * kATile + arow;
-          unsigned char* al = st + (tau * 2 + 1) * kATile + arow;
-          *(float4*)ah = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *(float4*)(ah + kALbo) = make_float4(hi[4], hi[5], hi[6], hi[7]);
-          *(float4*)al = make_float4(lo[0], lo[1], lo[2], lo[3]);
-          *(float4*)(al + kALbo) = make_float4(lo[4], lo[5], lo[6], lo[7]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (tid == 0) {
-            const int d = it / kNKB;
-            const uint32_t bytes = (uint32_t)(T.opk[kb + 1] - T.opk[kb]);
+            const int d = it / kSPO, kb = kb0;
+            const uint32_t bytes = (uint32_t)(T.opk[kb + kKPS] - T.opk[kb]);
             mbar_arrive_tx(&full[s], bytes);
             bulk_g2s(st + kAStage, A.op + (size_t)d * T.opk[kNKB] + T.opk[kb], bytes, &full[s]);
           } else {
@@ -614,24 +628,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
     const uint32_t idesc0 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 4) << 24);
     for (int it = 0; it < nit; ++it) {
       const int s = it % kStages;
-      const int kb = it - kNKB * (it / kNKB);
+      const int kb0 = (it - kSPO * (it / kSPO)) * kKPS;
       const int chunk = it / CN, cit = it - CN * chunk;   // cit = 0 restarts the chunk's accumulators
       if (cit == 0 && chunk >= 1) mbar_wait(&drained[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
       mbar_wait(&full[s], (it / kStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t st = saddr(smem + (size_t)s * kStage);
-      const int nc = T.ncols[kb];
-      const uint32_t idesc = idesc0 | ((uint32_t)(nc >> 3) << 17);
-      const uint64_t bh = umma_desc(st + kAStage, nc / 8 * 128);
-      const uint64_t bl = umma_desc(st + kAStage + nc * kKB * 4, nc / 8 * 128);
 #pragma unroll
-      for (int tau = 0; tau < kAcc; ++tau) {
-        const uint64_t ah = umma_desc(st + (tau * 2 + 0) * kATile, 16 * 128);
-        const uint64_t al = umma_desc(st + (tau * 2 + 1) * kATile, 16 * 128);
-        const uint32_t dt = tmem + (uint32_t)(tau * 128);
-        umma_tf32(dt, ah, bh, idesc, cit > 0 ? 1u : 0u);
-        umma_tf32(dt, al, bh, idesc, 1u);
-        umma_tf32(dt, ah, bl, idesc, 1u);
+      for (int b = 0; b < kKPS; ++b) {
+        const int kb = kb0 + b;
+        const int nc = T.ncols[kb];
+        const uint32_t boff = (uint32_t)(T.opk[kb] - T.opk[kb0]);
+        const uint32_t idesc = idesc0 | ((uint32_t)(nc >> 3) << 17);
+        const uint64_t bh = umma_desc(st + kAStage + boff, nc / 8 * 128);
+        const uint64_t bl = umma_desc(st + kAStage + boff + nc * kKB * 4, nc / 8 * 128);
+#pragma unroll
+        for (int tau = 0; tau < kAcc; ++tau) {
+          const uint64_t ah = umma_desc(st + ((b * kAcc + tau) * 2 + 0) * kATile, 16 * 128);
+          const uint64_t al = umma_desc(st + ((b * kAcc + tau) * 2 + 1) * kATile, 16 * 128);
+          const uint32_t dt = tmem + (uint32_t)(tau * 128);
+          umma_tf32(dt, ah, bh, idesc, (cit > 0 || b > 0) ? 1u : 0u);
+          umma_tf32(dt, al, bh, idesc, 1u);
+          umma_tf32(dt, ah, bl, idesc, 1u);
+        }
       }
       umma_commit(&empty[s]);
       if (cit == CN - 1 || it + 1 == nit) umma_commit(&chunk_full);
