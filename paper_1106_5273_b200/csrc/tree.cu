@@ -223,11 +223,29 @@ __global__ void k_local_flags(const int* __restrict__ leaf, const int* __restric
 __global__ void k_local_range(const int* __restrict__ level, const int* __restrict__ begin,
                               const int* __restrict__ count, int64_t nc, int64_t off, int64_t n,
                               int* __restrict__ lo, int* __restrict__ hi) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = begin[i], e = b + count[i];
-    if (b < off + n && e > off) {
-      atomicMin(&lo[level[i]], (int)i);
-      atomicMax(&hi[level[i]], (int)i);
+  // cells are level-ordered, so a warp's cells span at most a few levels:
+  // reduce within the warp per level before the atomics (one per warp and level
+  // instead of one per cell)
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; i0 < nc;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    bool in = false;
+    int lv = -1;
+    if (i < nc) {
+      const int64_t b = begin[i], e = b + count[i];
+      in = b < off + n && e > off;
+      lv = level[i];
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, in);
+    while (todo) {
+      const int l = __shfl_sync(0xffffffffu, lv, __ffs(todo) - 1);
+      const unsigned same = __ballot_sync(0xffffffffu, in && lv == l);
+      if (lane == __ffs(same) - 1) {
+        atomicMin(&lo[l], (int)(i0 + __ffs(same) - 1));
+        atomicMax(&hi[l], (int)(i0 + 31 - __clz(same)));
+      }
+      todo &= ~same;
     }
   }
 }

@@ -37,7 +37,7 @@ def summarise(path):
                         dram_GBps=b / t / 1e9 if t > 0 else 0.0,
                         fma_pipe_pct=a.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 0) / a["n"],
                         issue_pct=a.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) / a["n"],
-                        tensor_pct=a.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                        tensor_pct=a.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
                                          0) / a["n"]))
     return out, tot
 
