@@ -205,9 +205,11 @@ __device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A,
 }
 
 // leaf-local FP32 source data (a12 staging, once per evaluate): for every
-// particle of every leaf, (x - c_leaf) rounded from double, and 1/(2 sigma^2)
+// particle of every leaf, (x - c_leaf) rounded from double and w = 1/(2 sigma^2),
+// and sqrt(w) = 1/(sqrt2 sigma) in the free fourth lane of (alpha, .)
 __global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t ncells, double lo0, double lo1,
-                             double lo2, double L, const float4* __restrict__ pos, float4* __restrict__ posl) {
+                             double lo2, double L, const float4* __restrict__ pos, float4* __restrict__ posl,
+                             float4* __restrict__ alp) {
   const int lane = threadIdx.x & 31;
   for (int64_t cell = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; cell < ncells;
        cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -217,8 +219,9 @@ __global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t nce
     const int b = c.begin[cell], n = c.count[cell];
     for (int i = lane; i < n; i += 32) {
       const float4 p = pos[b + i];
-      posl[b + i] = make_float4((float)((double)p.x - cx), (float)((double)p.y - cy), (float)((double)p.z - cz),
-                                1.0f / (2.0f * p.w * p.w));
+      const float w = 1.0f / (2.0f * p.w * p.w);
+      posl[b + i] = make_float4((float)((double)p.x - cx), (float)((double)p.y - cy), (float)((double)p.z - cz), w);
+      alp[b + i].w = sqrtf(w);
     }
   }
 }
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
             const float4 a = alp[sb + j];
             const float w = p.w;
             const float qx = p.x + C0, qy = p.y + C1, qz = p.z + C2;
-            const float aw = sqrtf(w);
+            const float aw = a.w;                        // sqrt(w) (k_leaf_local)
             qv[h] = make_float4(qx, qy, qz, -1.4426950408889634f * w);
             av[h] = make_float4(a.x * k4, a.y * k4, a.z * k4, aw);
             wv[h] = make_float4(av[h].y * p.z - av[h].z * p.y, av[h].z * p.x - av[h].x * p.z,
@@ -399,7 +402,7 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   // the occupancy/unroll sweep on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8, <12,4,2> 210.2)
   c.posl.reserve(std::max<int64_t>(c.ntot, 1));
   FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
-             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p);
+             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p, c.alp.p);
   FMM_LAUNCH(c, (k_p2p<16, 4, 4>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
              c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
              c.dnear.p);

@@ -6,7 +6,7 @@
 #   latest_p2p.json  profiles/latest_p2p.json updated from the two (bench.py's roofline input)
 #   bench.json     the default bench line (N = 1, C3), run after the update
 #   launches.csv   ncu launch list (gpu__time_duration) of one bench step
-# usage: tools/profile_round.sh TAG "commit note"
+# usage: tools/profile_round.sh TAG "commit note" [light]   (light: skip the all-kernel and M2L captures)
 set -u
 TAG=$1; NOTE=${2:-}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
@@ -22,6 +22,7 @@ cp profiles/latest_p2p.json $OUT/latest_p2p.json
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $B > /dev/null 2>&1
 python tools/ncu_summary.py $OUT/launches.csv > $OUT/launches_summary.json 2>&1
+[ "${3:-}" = "light" ] && { echo done; exit 0; }
 # every kernel of one step with DRAM bytes, FMA / issue / tensor utilisation (HBM GB/s of keys, sort, tree)
 K="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"
 K=$K,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed
