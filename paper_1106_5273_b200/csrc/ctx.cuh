@@ -84,6 +84,12 @@ struct Ctx {
   // ---- lists (traversal) ----
   bool lists_valid = false;
   DBuf<uint64_t> p2p, m2l, sort_tmp, front_a, front_b;
+  DBuf<uint64_t> m2lr;                       // M2L entries the register kernels take, grouped by target
+  int64_t nm2lr = 0;
+  DBuf<int> dsel;                            // selected-count output of cub::DeviceSelect
+  DBuf<unsigned> tc_mask;                    // tensor-path verification: offset bitmask per cell
+  DBuf<unsigned char> tc_bad, tc_has;        // tc_has[t]: cell t has M2L entries (written by the traversal)
+  DBuf<int64_t> tc_off;
   DBuf<int> cnt_m2l, cnt_p2p, cnt_push, off_m2l, off_p2p, off_push;
   int64_t np2p = 0, nm2l = 0, p2p_pairs = 0;
   DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;
@@ -131,6 +137,7 @@ struct Ctx {
 // pipeline stages (each enqueues on ctx.stream; throws FmmError)
 void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const float* s);
 void build_lists(Ctx& c);
+void m2l_reg_segments(Ctx& c);
 void upward_pass(Ctx& c);
 void m2l_pass(Ctx& c);
 bool m2l_pass_reg(Ctx& c);

@@ -539,12 +539,15 @@ void upward_pass(Ctx& c) {
 void m2l_pass(Ctx& c) {
   if (c.nm2l == 0) return;
   // tensor-core M2L on the uniform levels (m2l_tc.cu), decided once per list build
-  if (!c.tc_valid) m2l_tc_prepare(c);
+  if (!c.tc_valid) {
+    m2l_tc_prepare(c);      // decides which targets the tensor path takes (verified entry by entry)
+    m2l_reg_segments(c);    // the remaining entries, grouped by target for the register kernels
+  }
   m2l_tc_run(c);
   if (m2l_pass_reg(c)) return;   // register-blocked kernel (m2l.cu) for p in {4, 6, 8, 10}
   int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   size_t sm = sizeof(float2) * (nc2 + 3 * nc);
-  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2l.p, gcells(c), geo(c), c.M.p,
+  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2lr.p, gcells(c), geo(c), c.M.p,
                                                           c.Lc.p);
   FMM_LAUNCH_CHECK();
 }

@@ -240,7 +240,7 @@ void launch_reg(Ctx& c) {
   size_t red = sizeof(float2) * (size_t)kSub * 3 * D::NC;
   if (red > sm) sm = red;
   MCells mc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, {c.per_units[0], c.per_units[1], c.per_units[2]}};
-  FMM_LAUNCH(c, k_m2l_reg<P>, (unsigned)c.ncells, 32, sm, c.m2l_b.p, c.m2l_e.p, c.m2l.p, mc, c.M.p, c.Lc.p,
+  FMM_LAUNCH(c, k_m2l_reg<P>, (unsigned)c.ncells, 32, sm, c.m2l_b.p, c.m2l_e.p, c.m2lr.p, mc, c.M.p, c.Lc.p,
              c.tc_skip.p);
 }
 

@@ -44,11 +44,15 @@
 // commits to the stage's "empty" mbarrier.  Targets are processed in Morton order so concurrently running
 // CTAs share their sources in L2.
 //
-// Which cells take this path is decided per list build: a reference cell
-// fixes the level's canonical offsets; a verification kernel checks for every
-// cell that its list, reflected into class 0, is exactly that set and that the
-// source the tensor kernel computes (Morton index of the offset cell in the
-// level-ordered cell array) is the list's source.  Cells that fail (adaptive
+// Which cells take this path is decided per list build, on the unsorted list
+// (two passes over it): the first cell of each level with entries fixes the
+// level's canonical offsets; every entry is then checked -- its offset,
+// reflected into class 0, is in that set, the source the tensor kernel
+// computes (Morton index of the offset cell in the level-ordered cell array)
+// is the entry's source, and its bit in the target's offset mask was not yet
+// set -- and a cell is taken iff none of its entries failed and its mask holds
+// all D offsets.  Only the remaining entries are grouped by target (for the
+// register kernel), so the big M2L list is never sorted.  Cells that fail (adaptive
 // trees, partial levels) stay on the register kernel (m2l.cu), which skips
 // the cells taken here.
 #include <algorithm>
@@ -301,55 +305,97 @@ TcTables make_tables() {
   return T;
 }
 
-// codes of one cell's entries (the level's reference cell)
-__global__ void k_tc_ref_codes(const uint64_t* __restrict__ lst, const int* __restrict__ seg_b,
-                               const int* __restrict__ seg_e, int cell, int lt, TcGeo g, int* __restrict__ out) {
-  long long ct[3];
-  centre(g, cell, lt, ct);
-  const int b = seg_b[cell], e = seg_e[cell];
-  for (int i = b + threadIdx.x; i < e; i += blockDim.x) out[i - b] = entry_code(g, lt, ct, lst[i]);
+// ---- per-build verification on the unsorted M2L list (emission order) ----
+// Every level's parameters at once, so each kernel is one pass over the list.
+struct TcVer {
+  int nlv;
+  int lt[kMaxTcLevels], lb[kMaxTcLevels], le[kMaxTcLevels], D[kMaxTcLevels], R[kMaxTcLevels], W[kMaxTcLevels];
+  int ref[kMaxTcLevels];
+  int64_t tbl_off[kMaxTcLevels], mask_off[kMaxTcLevels];
+};
+__device__ __forceinline__ int ver_level(const TcVer& v, int t) {
+  for (int k = 0; k < v.nlv; ++k)
+    if (t >= v.lb[k] && t < v.le[k]) return k;
+  return -1;
 }
 
-// first cell of [lb, le) with a non-empty list
-__global__ void k_tc_first(const int* __restrict__ seg_b, const int* __restrict__ seg_e, int lb, int le,
-                           int* __restrict__ out) {
+// first cell of [lb, le) with M2L entries (has[] is written by the traversal)
+__global__ void k_tc_first(const unsigned char* __restrict__ has, int lb, int le, int* __restrict__ out) {
   for (int c = lb + blockIdx.x * blockDim.x + threadIdx.x; c < le; c += gridDim.x * blockDim.x)
-    if (seg_e[c] > seg_b[c]) atomicMin(out, c);
+    if (has[c]) {
+      atomicMin(out, c);
+      return;                    // later cells of this thread are larger
+    }
 }
 
-// per cell: its list, reflected into class 0, is exactly the canonical offset
-// set and every source is the one tc_source computes.  Warp per cell; ok
-// cells are appended to tgt (sorted afterwards).
-__global__ void k_tc_verify(const uint64_t* __restrict__ lst, const int* __restrict__ seg_b,
-                            const int* __restrict__ seg_e, int lb, int le, int lt, int D, TcGeo g,
-                            const short* __restrict__ tbl, int R, unsigned char* __restrict__ skip,
-                            int* __restrict__ tgt, int* __restrict__ ntgt) {
-  const int lane = threadIdx.x & 31;
-  const int V = 2 * R + 1;
-  for (int c = lb + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); c < le;
-       c += (int)((gridDim.x * blockDim.x) >> 5)) {
-    const int cls = parity_class(g, c);
-    const int b = seg_b[c], e = seg_e[c];
-    bool ok = (e - b) == D;
-    long long ct[3];
-    centre(g, c, lt, ct);
-    for (int i = b + lane; ok && i < e; i += 32) {
-      const uint64_t ent = lst[i];
-      const int code = entry_code(g, lt, ct, ent);
-      bool good = code >= 0;
-      if (good) {
-        const int c0 = reflect(code, cls);
-        const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
-        good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
-        if (good) good = tbl[(((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R] >= 0;
-        if (good) good = tc_source(g, lt, ct, code) == (int)((ent >> 5) & 0x7ffffff);
-      }
-      ok = ok && good;
+// the reference cells' entries as offset codes (appended per level; the
+// order is irrelevant, the host sorts them)
+__global__ void k_tc_ref_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g, int cap,
+                                 int* __restrict__ codes, int* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t ent = lst[i];
+    const int t = (int)(ent >> 32);
+    for (int k = 0; k < v.nlv; ++k) {
+      if (t != v.ref[k]) continue;
+      long long ct[3];
+      centre(g, t, v.lt[k], ct);
+      const int j = atomicAdd(&cnt[k], 1);
+      if (j < cap) codes[(int64_t)k * cap + j] = entry_code(g, v.lt[k], ct, ent);
     }
-    ok = __all_sync(0xffffffffu, ok);
-    if (lane == 0 && ok) {
-      skip[c] = 1;
-      tgt[atomicAdd(ntgt, 1)] = c;
+  }
+}
+
+// per entry whose target is in a candidate level: its offset, reflected into
+// class 0, is in the canonical table and its source is the one tc_source
+// computes; the offset's bit is set in the target's mask (a bit already set
+// is a duplicate).  Any failure marks the target bad.
+__global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
+                                    const short* __restrict__ tbl, unsigned* __restrict__ mask,
+                                    unsigned char* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t ent = lst[i];
+    const int t = (int)(ent >> 32);
+    const int k = ver_level(v, t);
+    if (k < 0) continue;
+    const int lt = v.lt[k], R = v.R[k], V = 2 * R + 1;
+    long long ct[3];
+    centre(g, t, lt, ct);
+    const int code = entry_code(g, lt, ct, ent);
+    bool good = code >= 0;
+    int d = -1;
+    if (good) {
+      const int c0 = reflect(code, parity_class(g, t));
+      const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
+      good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
+      if (good) d = tbl[v.tbl_off[k] + (((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R];
+      good = good && d >= 0;
+    }
+    if (good) good = tc_source(g, lt, ct, code) == (int)((ent >> 5) & 0x7ffffff);
+    const int64_t row = (int64_t)(t - v.lb[k]);
+    if (good) {
+      const unsigned bit = 1u << (d & 31);
+      const unsigned old = atomicOr(&mask[v.mask_off[k] + row * v.W[k] + (d >> 5)], bit);
+      good = !(old & bit);
+    }
+    if (!good) bad[v.lb[k] + row] = 1;
+  }
+}
+
+// per cell of the candidate levels: all D canonical offsets present exactly
+// once and no bad entry -> taken by the tensor path (appended per level)
+__global__ void k_tc_accept(TcVer v, const unsigned* __restrict__ mask, const unsigned char* __restrict__ bad,
+                            unsigned char* __restrict__ skip, int* __restrict__ tgt, const int64_t* __restrict__ tgt_off,
+                            int* __restrict__ ntgt) {
+  for (int k = 0; k < v.nlv; ++k) {
+    for (int c = v.lb[k] + (int)(blockIdx.x * blockDim.x + threadIdx.x); c < v.le[k]; c += (int)(gridDim.x * blockDim.x)) {
+      if (bad[c]) continue;
+      int pc = 0;
+      const unsigned* m = mask + v.mask_off[k] + (int64_t)(c - v.lb[k]) * v.W[k];
+      for (int w = 0; w < v.W[k]; ++w) pc += __popc(m[w]);
+      if (pc == v.D[k]) {
+        skip[c] = 1;
+        tgt[tgt_off[k] + atomicAdd(&ntgt[k], 1)] = c;
+      }
     }
   }
 }
@@ -700,33 +746,50 @@ void m2l_tc_prepare(Ctx& c) {
   cudaStream_t st = c.stream;
   struct Cand { int lt, D, R; std::vector<int> codes; std::vector<short> tbl; };
   std::vector<Cand> cands;
-  c.tc_tmp.reserve(4);
+  // the first cell with M2L entries in every level (the reference cells)
+  std::vector<int> first(kMaxLevel + 2, 0x7fffffff);
+  c.tc_tmp.reserve(kMaxLevel + 2);
+  FMM_CUDA(cudaMemcpyAsync(c.tc_tmp.p, first.data(), sizeof(int) * first.size(), cudaMemcpyHostToDevice, st));
   for (int l = 2; l < nlev; ++l) {
     const int lb = (int)c.level_begin[l], le = (int)c.level_begin[l + 1];
+    if (le - lb >= 1024) FMM_LAUNCH(c, k_tc_first, 148, 256, 0, c.tc_has.p, lb, le, c.tc_tmp.p + l);
+  }
+  FMM_CUDA(cudaMemcpyAsync(first.data(), c.tc_tmp.p, sizeof(int) * first.size(), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  const unsigned gl = (unsigned)std::min<int64_t>((c.nm2l + 255) / 256, 148 * 16);
+  TcVer v{};
+  for (int l = 2; l < nlev && v.nlv < kMaxTcLevels; ++l) {
+    const int lb = (int)c.level_begin[l], le = (int)c.level_begin[l + 1];
     if (le - lb < 1024) continue;       // small levels: the register kernel is as fast
-    int ref = 0x7fffffff;
-    FMM_CUDA(cudaMemcpyAsync(c.tc_tmp.p, &ref, sizeof(int), cudaMemcpyHostToDevice, st));
-    FMM_LAUNCH(c, k_tc_first, 148, 256, 0, c.m2l_b.p, c.m2l_e.p, lb, le, c.tc_tmp.p);
-    FMM_CUDA(cudaMemcpyAsync(&ref, c.tc_tmp.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaStreamSynchronize(st));
-    if (ref == 0x7fffffff) continue;
-    int be[2] = {0, 0}, hq[3] = {0, 0, 0};
-    FMM_CUDA(cudaMemcpyAsync(&be[0], c.m2l_b.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaMemcpyAsync(&be[1], c.m2l_e.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (first[l] == 0x7fffffff) continue;
+    v.lt[v.nlv] = l;
+    v.ref[v.nlv] = first[l];
+    ++v.nlv;
+  }
+  if (v.nlv == 0) return;
+  // one pass: the reference cells' offset codes
+  constexpr int kCap = 8192;
+  c.tc_codes_tmp.reserve((int64_t)kCap * v.nlv);
+  c.tc_cnt.reserve(kMaxTcLevels);
+  FMM_CUDA(cudaMemsetAsync(c.tc_cnt.p, 0, sizeof(int) * kMaxTcLevels, st));
+  FMM_LAUNCH(c, k_tc_ref_entries, gl, 256, 0, c.m2l.p, c.nm2l, v, g, kCap, c.tc_codes_tmp.p, c.tc_cnt.p);
+  std::vector<int> rcnt(kMaxTcLevels);
+  std::vector<int> rcodes((size_t)kCap * v.nlv);
+  FMM_CUDA(cudaMemcpyAsync(rcnt.data(), c.tc_cnt.p, sizeof(int) * kMaxTcLevels, cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(rcodes.data(), c.tc_codes_tmp.p, sizeof(int) * rcodes.size(), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < v.nlv; ++k) {
+    const int l = v.lt[k], ref = v.ref[k], D = rcnt[k];
+    if (D <= 0 || D > kCap) continue;
+    int hq[3] = {0, 0, 0};
     FMM_CUDA(cudaMemcpyAsync(&hq[0], c.cells.qx.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
     FMM_CUDA(cudaMemcpyAsync(&hq[1], c.cells.qy.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
     FMM_CUDA(cudaMemcpyAsync(&hq[2], c.cells.qz.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
     FMM_CUDA(cudaStreamSynchronize(st));
-    const int D = be[1] - be[0];
-    if (D <= 0 || D > 8192) continue;
-    c.tc_codes_tmp.reserve(D);
-    FMM_LAUNCH(c, k_tc_ref_codes, 1, 256, 0, c.m2l.p, c.m2l_b.p, c.m2l_e.p, ref, l, g, c.tc_codes_tmp.p);
     Cand cd;
     cd.lt = l;
     cd.D = D;
-    cd.codes.resize(D);
-    FMM_CUDA(cudaMemcpyAsync(cd.codes.data(), c.tc_codes_tmp.p, sizeof(int) * D, cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaStreamSynchronize(st));
+    cd.codes.assign(rcodes.begin() + (size_t)k * kCap, rcodes.begin() + (size_t)k * kCap + D);
     if (*std::min_element(cd.codes.begin(), cd.codes.end()) < 0) continue;
     // canonical (class 0) offsets: the reference cell's, reflected from its class
     const int rcls = (hq[0] & 1) | ((hq[1] & 1) << 1) | ((hq[2] & 1) << 2);
@@ -747,34 +810,46 @@ void m2l_tc_prepare(Ctx& c) {
     cands.push_back(std::move(cd));
   }
   if (cands.empty()) return;
-  // verify every cell of the candidate levels; collect and sort the targets
-  int64_t tgt_total = 0, code_total = 0, op_total = 0;
-  for (auto& cd : cands) {
-    tgt_total += c.level_begin[cd.lt + 1] - c.level_begin[cd.lt];
+  // one pass: verify every entry of the candidate levels' targets, then accept
+  // the cells whose list is exactly the canonical set
+  int64_t tgt_total = 0, code_total = 0, op_total = 0, tbl_total = 0, mask_total = 0;
+  TcVer w{};
+  w.nlv = (int)cands.size();
+  std::vector<int64_t> tgt_off, code_off;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    auto& cd = cands[i];
+    const int lb = (int)c.level_begin[cd.lt], le = (int)c.level_begin[cd.lt + 1];
+    w.lt[i] = cd.lt; w.lb[i] = lb; w.le[i] = le; w.D[i] = cd.D; w.R[i] = cd.R; w.W[i] = (cd.D + 31) / 32;
+    w.tbl_off[i] = tbl_total;
+    w.mask_off[i] = mask_total;
+    tgt_off.push_back(tgt_total);
+    code_off.push_back(code_total);
+    tbl_total += (int64_t)cd.tbl.size();
+    mask_total += (int64_t)(le - lb) * w.W[i];
+    tgt_total += le - lb;
     code_total += cd.D;
   }
   c.tc_tgt.reserve(tgt_total);
   c.tc_tgt2.reserve(tgt_total);
   c.tc_codes.reserve(code_total);
-  c.tc_cnt.reserve(cands.size());
-  FMM_CUDA(cudaMemsetAsync(c.tc_cnt.p, 0, sizeof(int) * cands.size(), st));
-  int64_t toff = 0, coff = 0;
-  std::vector<int64_t> tgt_off, code_off;
+  c.tc_tbl.reserve(tbl_total);
+  c.tc_mask.reserve(mask_total);
+  c.tc_bad.reserve(std::max<int64_t>(c.ncells, 1));
+  FMM_CUDA(cudaMemsetAsync(c.tc_mask.p, 0, sizeof(unsigned) * mask_total, st));
+  FMM_CUDA(cudaMemsetAsync(c.tc_bad.p, 0, std::max<int64_t>(c.ncells, 1), st));
+  FMM_CUDA(cudaMemsetAsync(c.tc_cnt.p, 0, sizeof(int) * kMaxTcLevels, st));
   for (size_t i = 0; i < cands.size(); ++i) {
-    auto& cd = cands[i];
-    const int lb = (int)c.level_begin[cd.lt], le = (int)c.level_begin[cd.lt + 1];
-    c.tc_tbl.reserve(cd.tbl.size());
-    FMM_CUDA(cudaMemcpyAsync(c.tc_tbl.p, cd.tbl.data(), sizeof(short) * cd.tbl.size(), cudaMemcpyHostToDevice, st));
-    FMM_CUDA(cudaMemcpyAsync(c.tc_codes.p + coff, cd.codes.data(), sizeof(int) * cd.D, cudaMemcpyHostToDevice, st));
-    const unsigned blocks = (unsigned)std::min<int64_t>((le - lb + 7) / 8, 148 * 16);
-    FMM_LAUNCH(c, k_tc_verify, blocks, 256, 0, c.m2l.p, c.m2l_b.p, c.m2l_e.p, lb, le, cd.lt, cd.D, g, c.tc_tbl.p, cd.R,
-               c.tc_skip.p, c.tc_tgt.p + toff, c.tc_cnt.p + i);
-    FMM_CUDA(cudaStreamSynchronize(st));    // the table buffer is reused by the next level
-    tgt_off.push_back(toff);
-    code_off.push_back(coff);
-    toff += le - lb;
-    coff += cd.D;
+    FMM_CUDA(cudaMemcpyAsync(c.tc_tbl.p + w.tbl_off[i], cands[i].tbl.data(), sizeof(short) * cands[i].tbl.size(),
+                             cudaMemcpyHostToDevice, st));
+    FMM_CUDA(cudaMemcpyAsync(c.tc_codes.p + code_off[i], cands[i].codes.data(), sizeof(int) * cands[i].D,
+                             cudaMemcpyHostToDevice, st));
   }
+  c.tc_off.reserve(kMaxTcLevels);
+  FMM_CUDA(cudaMemcpyAsync(c.tc_off.p, tgt_off.data(), sizeof(int64_t) * tgt_off.size(), cudaMemcpyHostToDevice, st));
+  FMM_LAUNCH(c, k_tc_verify_entries, gl, 256, 0, c.m2l.p, c.nm2l, w, g, c.tc_tbl.p, c.tc_mask.p, c.tc_bad.p);
+  FMM_LAUNCH(c, k_tc_accept, 148 * 4, 256, 0, w, c.tc_mask.p, c.tc_bad.p, c.tc_skip.p, c.tc_tgt.p, c.tc_off.p,
+             c.tc_cnt.p);
+  FMM_CUDA(cudaStreamSynchronize(st));    // host vectors above are read by the copies
   std::vector<int> cnt(cands.size());
   FMM_CUDA(cudaMemcpyAsync(cnt.data(), c.tc_cnt.p, sizeof(int) * cands.size(), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));

@@ -61,7 +61,8 @@ template <bool WRITE>
 __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells c, TParams p,
                          int* __restrict__ cm, int* __restrict__ cp, int* __restrict__ cq,
                          const int* __restrict__ om, const int* __restrict__ op, const int* __restrict__ oq,
-                         uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p, uint64_t* __restrict__ next) {
+                         uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p, uint64_t* __restrict__ next,
+                         unsigned char* __restrict__ has_m2l) {
   int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f >= nf) return;
   uint64_t e = front[f];
@@ -77,7 +78,10 @@ __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells 
     int b = split_b ? cb + k : B;
     if (!split_b && !c.tgt_ok[a]) continue;        // a14: targets of other ranks are theirs
     int d = interact(c, p, a, b, img);
-    if (d == 0) { if (WRITE) m2l[bm + nm] = pack(a, b, img); ++nm; }
+    if (d == 0) {
+      if (WRITE) { m2l[bm + nm] = pack(a, b, img); has_m2l[a] = 1; }   // has_m2l: for m2l_tc_prepare
+      ++nm;
+    }
     else if (d == 1) { if (WRITE) p2p[bp + np] = pack(a, b, img); ++np; }
     else { if (WRITE) next[bq + nq] = pack(a, b, img); ++nq; }
   }
@@ -143,6 +147,38 @@ void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
 
 }  // namespace
 
+struct NotOnTensorPath {
+  const unsigned char* skip;
+  __device__ __forceinline__ bool operator()(const uint64_t& e) const { return !skip[(int)(e >> 32)]; }
+};
+
+// the M2L entries whose target the tensor path did not take (tc_skip == 0),
+// in emission order (stable select), grouped by target (stable sort), with
+// per-target segments m2l_b/m2l_e for the register kernels
+void m2l_reg_segments(Ctx& c) {
+  cudaStream_t st = c.stream;
+  c.nm2lr = 0;
+  c.m2l_b.reserve(std::max<int64_t>(c.ncells, 1)); c.m2l_e.reserve(std::max<int64_t>(c.ncells, 1));
+  FMM_LAUNCH(c, k_clear2, nblocks(std::max<int64_t>(c.ncells, 1), 256), 256, 0, c.m2l_b.p, c.m2l_e.p, c.ncells);
+  if (c.nm2l == 0) return;
+  c.m2lr.reserve(c.nm2l);
+  c.dsel.reserve(1);
+  const uint64_t* in = c.m2l.p;
+  uint64_t* out = c.m2lr.p;
+  int* nsel = c.dsel.p;
+  const int n = (int)c.nm2l;
+  NotOnTensorPath pred{c.tc_skip.p};
+  cub_call(c, [&](void* tmp, size_t& bytes) {
+    return cub::DeviceSelect::If(tmp, bytes, in, out, nsel, n, pred, st);
+  });
+  int ns = 0;
+  FMM_CUDA(cudaMemcpyAsync(&ns, c.dsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c.nm2lr = ns;
+  sort_list(c, c.m2lr, c.nm2lr, 32);
+  if (c.nm2lr) FMM_LAUNCH(c, k_segments, nblocks(c.nm2lr, 256), 256, 0, c.m2lr.p, c.nm2lr, c.m2l_b.p, c.m2l_e.p);
+}
+
 void build_lists(Ctx& c) {
   c.tc_valid = false;
   cudaStream_t st = c.stream;
@@ -166,6 +202,8 @@ void build_lists(Ctx& c) {
   int64_t nf = (int64_t)seeds.size();
   c.front_a.reserve(1024);
   c.front_b.reserve(1024);
+  c.tc_has.reserve(std::max<int64_t>(c.ncells, 1));
+  FMM_CUDA(cudaMemsetAsync(c.tc_has.p, 0, std::max<int64_t>(c.ncells, 1), st));
   c.p2p.reserve(1 << 16);
   c.m2l.reserve(1 << 16);
   if (root_leaf) {
@@ -181,7 +219,7 @@ void build_lists(Ctx& c) {
     c.off_m2l.reserve(nf + 1); c.off_p2p.reserve(nf + 1); c.off_push.reserve(nf + 1);
     unsigned g = nblocks(nf, 256);
     FMM_LAUNCH(c, k_expand<false>, g, 256, 0, c.front_a.p, nf, tc, tp, c.cnt_m2l.p, c.cnt_p2p.p, c.cnt_push.p,
-                                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+                                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     FMM_LAUNCH_CHECK();
     exclusive_scan(c, c.cnt_m2l.p, c.off_m2l.p, nf);
     exclusive_scan(c, c.cnt_p2p.p, c.off_p2p.p, nf);
@@ -201,7 +239,8 @@ void build_lists(Ctx& c) {
     c.p2p.grow_keep(c.np2p + add_p, c.np2p, st);
     c.front_b.reserve(add_q);
     FMM_LAUNCH(c, k_expand<true>, g, 256, 0, c.front_a.p, nf, tc, tp, nullptr, nullptr, nullptr, c.off_m2l.p,
-                                      c.off_p2p.p, c.off_push.p, c.m2l.p + c.nm2l, c.p2p.p + c.np2p, c.front_b.p);
+                                      c.off_p2p.p, c.off_push.p, c.m2l.p + c.nm2l, c.p2p.p + c.np2p, c.front_b.p,
+                                      c.tc_has.p);
     FMM_LAUNCH_CHECK();
     c.nm2l += add_m;
     c.np2p += add_p;
@@ -211,16 +250,15 @@ void build_lists(Ctx& c) {
   }
 
   // per-target segments: P2P in canonical order (it fixes the near-field
-  // summation order, identical on 1 and N GPUs), M2L grouped by target only
-  // (half the radix passes; fmm_get_lists returns the canonical order)
+  // summation order, identical on 1 and N GPUs).  The M2L list stays in the
+  // traversal's (deterministic) emission order: the tensor path verifies it
+  // entry by entry, and only the entries it does not take are grouped by
+  // target for the register kernels (m2l_reg_segments, after m2l_tc_prepare);
+  // fmm_get_lists returns the canonical order
   sort_list(c, c.p2p, c.np2p);
-  sort_list(c, c.m2l, c.nm2l, 32);
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
-  c.m2l_b.reserve(c.ncells); c.m2l_e.reserve(c.ncells);
   FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
-  FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.m2l_b.p, c.m2l_e.p, c.ncells);
   if (c.np2p) FMM_LAUNCH(c, k_segments, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
-  if (c.nm2l) FMM_LAUNCH(c, k_segments, nblocks(c.nm2l, 256), 256, 0, c.m2l.p, c.nm2l, c.m2l_b.p, c.m2l_e.p);
   c.dcount.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
   if (c.np2p) {
