@@ -79,12 +79,16 @@ __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells 
     if (!split_b && !c.tgt_ok[a]) continue;        // a14: targets of other ranks are theirs
     int d = interact(c, p, a, b, img);
     if (d == 0) {
-      if (WRITE) { m2l[bm + nm] = pack(a, b, img); has_m2l[a] = 1; }   // has_m2l: for m2l_tc_prepare
+      if (WRITE) {
+        m2l[bm + nm] = pack(a, b, img);
+        if (!split_b) has_m2l[a] = 1;              // has_m2l: for m2l_tc_prepare (A's flag: below)
+      }
       ++nm;
     }
     else if (d == 1) { if (WRITE) p2p[bp + np] = pack(a, b, img); ++np; }
     else { if (WRITE) next[bq + nq] = pack(a, b, img); ++nq; }
   }
+  if (WRITE && split_b && nm > 0) has_m2l[A] = 1;
   if (!WRITE) { cm[f] = nm; cp[f] = np; cq[f] = nq; }
 }
 
