@@ -90,6 +90,7 @@ struct Ctx {
   DBuf<unsigned> tc_mask;                    // tensor-path verification: offset bitmask per cell
   DBuf<unsigned char> tc_bad, tc_has;        // tc_has[t]: cell t has M2L entries (written by the traversal)
   DBuf<int64_t> tc_off;
+  DBuf<int4> tc_cq;                          // packed (qx, qy, qz, level) for the verification
   DBuf<int> cnt_m2l, cnt_p2p, cnt_push, off_m2l, off_p2p, off_push;
   int64_t np2p = 0, nm2l = 0, p2p_pairs = 0;
   DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;

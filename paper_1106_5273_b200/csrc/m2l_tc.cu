@@ -172,6 +172,7 @@ __host__ __device__ __forceinline__ float tf32_hi(float x) {
 // ------------------------------------------------------------ geometry ----
 struct TcGeo {
   const int *qx, *qy, *qz, *level;
+  const int4* cq;                   // (qx, qy, qz, level) per cell, packed per list build (verification)
   long long per[3];                 // periods in half-finest-cell units
   int lvl_begin[kMaxLevel + 2];
 };
@@ -231,6 +232,29 @@ __device__ __forceinline__ int entry_code(const TcGeo& g, int lt, const long lon
     const long long cs = (long long)(2 * qs[a] + 1) << (kMaxLevel - ls);
     const long long d = ct[a] - cs - (long long)im[a] * g.per[a];
     const int sh = kMaxLevel - lf;                  // Delta is a multiple of 2^sh for a valid entry
+    if (d & ((1ll << sh) - 1)) return -1;
+    const long long v = d >> sh;
+    if (v < -63 || v > 63) return -1;
+    code |= (int)(v + 64) << (14 - 7 * a);
+  }
+  return code;
+}
+
+// the same from the packed cell table: one 16-byte load per cell
+__device__ __forceinline__ int entry_code4(const TcGeo& g, int lt, const long long (&ct)[3], uint64_t ent) {
+  const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
+  const int4 sq = __ldg(g.cq + src);
+  const int ls = sq.w, dl = ls - lt;
+  if (dl < -1 || dl > 1) return -1;
+  const int lf = max(lt, ls);
+  const int qs[3] = {sq.x, sq.y, sq.z};
+  const int im[3] = {img % 3 - 1, (img / 3) % 3 - 1, img / 9 - 1};
+  int code = (dl + 1) << 21;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long cs = (long long)(2 * qs[a] + 1) << (kMaxLevel - ls);
+    const long long d = ct[a] - cs - (long long)im[a] * g.per[a];
+    const int sh = kMaxLevel - lf;
     if (d & ((1ll << sh) - 1)) return -1;
     const long long v = d >> sh;
     if (v < -63 || v > 63) return -1;
@@ -358,13 +382,16 @@ __global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n,
     const int k = ver_level(v, t);
     if (k < 0) continue;
     const int lt = v.lt[k], R = v.R[k], V = 2 * R + 1;
+    const int4 tq = __ldg(g.cq + t);
     long long ct[3];
-    centre(g, t, lt, ct);
-    const int code = entry_code(g, lt, ct, ent);
+    ct[0] = (long long)(2 * tq.x + 1) << (kMaxLevel - lt);
+    ct[1] = (long long)(2 * tq.y + 1) << (kMaxLevel - lt);
+    ct[2] = (long long)(2 * tq.z + 1) << (kMaxLevel - lt);
+    const int code = entry_code4(g, lt, ct, ent);
     bool good = code >= 0;
     int d = -1;
     if (good) {
-      const int c0 = reflect(code, parity_class(g, t));
+      const int c0 = reflect(code, (tq.x & 1) | ((tq.y & 1) << 1) | ((tq.z & 1) << 2));
       const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
       good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
       if (good) d = tbl[v.tbl_off[k] + (((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R];
@@ -708,9 +735,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 128));
 }
 
+__global__ void k_tc_cq(const int* __restrict__ qx, const int* __restrict__ qy, const int* __restrict__ qz,
+                        const int* __restrict__ level, int64_t n, int4* __restrict__ cq) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cq[i] = make_int4(qx[i], qy[i], qz[i], level[i]);
+}
+
 TcGeo make_geo(Ctx& c) {
   TcGeo g{};
   g.qx = c.cells.qx.p; g.qy = c.cells.qy.p; g.qz = c.cells.qz.p; g.level = c.cells.level.p;
+  g.cq = c.tc_cq.p;
   for (int a = 0; a < 3; ++a) g.per[a] = c.per_units[a];
   const int nl = (int)c.level_begin.size();
   for (int l = 0; l < kMaxLevel + 2; ++l) g.lvl_begin[l] = (int)c.level_begin[std::min(l, nl - 1)];
@@ -741,6 +775,9 @@ void m2l_tc_prepare(Ctx& c) {
     if (c.per_units[a] & (c.per_units[a] - 1)) return;       // tc_source wraps with a mask
   const int nlev = (int)c.level_begin.size() - 1;
   if (nlev > 11) return;                                    // 10-bit Morton spread in tc_source
+  c.tc_cq.reserve(std::max<int64_t>(c.ncells, 1));
+  FMM_LAUNCH(c, k_tc_cq, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
+             c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, c.tc_cq.p);
   const TcGeo g = make_geo(c);
   const TcTables T = make_tables();
   cudaStream_t st = c.stream;
