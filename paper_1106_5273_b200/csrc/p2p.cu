@@ -7,7 +7,7 @@
 // (readings Z1, Z3, Z4, Z7).  sum_j f (alpha_j x alpha_i) is
 // accumulated as (sum_j f alpha_j) x alpha_i.
 //
-// Mapping (sm_100a, FP32-issue bound): one warp per target leaf, two target
+// Mapping (sm_100a, bound by the FP32 FMA pipe: 75.8% busy at C3, r01 v19): one warp per target leaf, two target
 // particles per lane held in registers, so every shared-memory source load
 // feeds two pair evaluations.  Each source leaf of the target's segment is
 // staged in shared memory as float4 tiles in *target-leaf-centred*
