@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--full", action="store_true", help="also time full evaluate phases")
     ap.add_argument("--m2l-path", type=int, default=0)
+    ap.add_argument("--save", default="", help="save variant 0's (u, d) here (.npy) for an A/B of two FMM_LIB builds")
     args = ap.parse_args()
     import torch
     import paper_1106_5273_b200 as P
@@ -43,6 +44,8 @@ def main():
         out = torch.cat([u, d], 1).cpu().numpy()
         if ref is None:
             ref = out
+            if args.save:
+                np.save(args.save, out)
         diff = float(np.abs(out - ref).max() / np.abs(ref).max())
         print("variant %d  p2p %.2f ms (min %.2f)  max rel diff vs v0 %.2e" % (v, statistics.median(ms), min(ms), diff),
               flush=True)
