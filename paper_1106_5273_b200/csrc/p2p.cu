@@ -293,51 +293,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
     }
 #pragma unroll
     for (int q = 0; q < kDQ; ++q) sD[q][lane] = 0.0;
-#if P2P_PF
-    // P2P_PF (development variant): the next list entry's cell-table reads are
-    // issued before the current entry's tiles are evaluated, so the dependent
-    // chain lst -> cell table does not stall the warp at the tile boundary
-    int n_img = 0, n_lev = 0, n_qx = 0, n_qy = 0, n_qz = 0, n_sb = 0, n_cnt = 0;
-    auto fetch = [&](int e) {
-      const uint64_t ent = lst[e];
-      const int src = (int)((ent >> 5) & 0x7ffffff);
-      n_img = (int)(ent & 31);
-      n_lev = c.level[src]; n_qx = c.qx[src]; n_qy = c.qy[src]; n_qz = c.qz[src];
-      n_sb = c.begin[src]; n_cnt = c.count[src];
-    };
-    if (eb < ee) fetch(eb);
-#if P2P_PF >= 2
-    // P2P_PF = 2: also the first tile of the next entry's sources (two-deep
-    // cell-table pipeline: m_ = this entry, n_ = the next one)
-    float4 pp[2], pa[2];
-    auto fetch_p = [&](int sb, int cnt) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = lane + h * NT;
-        if (j < cnt) { pp[h] = posl[sb + j]; pa[h] = alp[sb + j]; }
-      }
-    };
-    if (eb < ee) fetch_p(n_sb, n_cnt);
-    int m_img = n_img, m_lev = n_lev, m_qx = n_qx, m_qy = n_qy, m_qz = n_qz, m_sb = n_sb, m_cnt = n_cnt;
-    if (eb + 1 < ee) fetch(eb + 1);
-#endif
-#endif
     for (int e = eb; e < ee; ++e) {
-#if P2P_PF >= 2
-      const int img = m_img, slev = m_lev, sqx = m_qx, sqy = m_qy, sqz = m_qz, sb = m_sb, scnt = m_cnt;
-      m_img = n_img; m_lev = n_lev; m_qx = n_qx; m_qy = n_qy; m_qz = n_qz; m_sb = n_sb; m_cnt = n_cnt;
-      if (e + 2 < ee) fetch(e + 2);
-      if (scnt == 0 && e + 1 < ee) fetch_p(m_sb, m_cnt);   // no tile below to issue it from
-#elif P2P_PF
-      const int img = n_img, slev = n_lev, sqx = n_qx, sqy = n_qy, sqz = n_qz, sb = n_sb, scnt = n_cnt;
-      if (e + 1 < ee) fetch(e + 1);
-#endif
-#if P2P_PF
-      const double ss = L / (double)(1 << slev);
-      const float C0 = (float)(lo0 + (sqx + 0.5) * ss + (img % 3 - 1) * px - cx);
-      const float C1 = (float)(lo1 + (sqy + 0.5) * ss + ((img / 3) % 3 - 1) * py - cy);
-      const float C2 = (float)(lo2 + (sqz + 0.5) * ss + (img / 9 - 1) * pz - cz);
-#else
       const uint64_t ent = lst[e];
       const int src = (int)((ent >> 5) & 0x7ffffff), img = (int)(ent & 31);
       // the source leaf centre in the target frame (image shift included), in
@@ -347,7 +303,6 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       const float C1 = (float)(lo1 + (c.qy[src] + 0.5) * ss + ((img / 3) % 3 - 1) * py - cy);
       const float C2 = (float)(lo2 + (c.qz[src] + 0.5) * ss + (img / 9 - 1) * pz - cz);
       const int sb = c.begin[src], scnt = c.count[src];
-#endif
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
         // stage the tile, far sources first: a source is "far" when it is
@@ -361,13 +316,8 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           vj[h] = j < scnt;
           fj[h] = false;
           if (vj[h]) {
-#if P2P_PF >= 2
-            const float4 p = s0 == 0 ? pp[h] : posl[sb + j];   // (y - C, 1/(2 sigma^2))
-            const float4 a = s0 == 0 ? pa[h] : alp[sb + j];
-#else
             const float4 p = posl[sb + j];               // (y - C, 1/(2 sigma^2))
             const float4 a = alp[sb + j];
-#endif
             const float w = p.w;
             const float qx = p.x + C0, qy = p.y + C1, qz = p.z + C2;
             const float aw = a.w;                        // sqrt(w) (k_leaf_local)
@@ -381,9 +331,6 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
             fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
           }
         }
-#if P2P_PF >= 2
-        if (s0 == 0 && e + 1 < ee) fetch_p(m_sb, m_cnt);   // consumed by the next entry's first tile
-#endif
         const unsigned lt = (1u << lane) - 1u;
         const unsigned f0 = __ballot_sync(0xffffffffu, fj[0]), f1 = __ballot_sync(0xffffffffu, fj[1]);
         const unsigned n0 = __ballot_sync(0xffffffffu, vj[0] && !fj[0]), n1 = __ballot_sync(0xffffffffu, vj[1] && !fj[1]);
@@ -453,6 +400,9 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   // 16 blocks/SM (128 registers), far loop unrolled 4x, near 4x: the best of
   // the occupancy/unroll sweep on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8, <12,4,2> 210.2)
+  // Prefetching the next list entry while the current tile is evaluated does not pay (r01 v23 A/B,
+  // tools/p2p_ab.sh, bit-identical results): its cell-table reads 200.35 -> 200.80 ms, plus its first
+  // source tile 207.53 ms (40 B of spills); the tile-boundary load latency is hidden by the other warps.
   c.posl.reserve(std::max<int64_t>(c.ntot, 1));
   FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
              (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p, c.alp.p);
