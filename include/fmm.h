@@ -29,6 +29,11 @@
  *  - Arrays: contiguous, row-major FP32.  A pointer may be device memory on
  *    cfg.device or host memory (pageable or pinned); the library detects which
  *    with cudaPointerGetAttributes and copies host data itself.
+ *  - Stream ordering: all work runs on cfg.stream.  With cfg.stream == NULL the
+ *    library creates a *blocking* stream, which is ordered with the legacy
+ *    default stream (where torch's default stream enqueues): inputs written
+ *    there are complete before the library reads them.  With a caller stream,
+ *    the caller orders its producers/consumers with that stream.
  *  - Ownership: the caller owns every array it passes.  set_particles copies
  *    its inputs and returns after validation; evaluate overwrites the caller's
  *    output arrays and returns when they are valid (stream synchronised).
@@ -110,7 +115,7 @@ typedef struct {
   int64_t  launches;             /* this library's kernel launches since set_particles */
   int64_t  cub_calls;            /* CUB device-wide calls (radix sort, scan) since then */
   int64_t  p2p_near_pairs;       /* pairs of P2P tiles evaluated with the cutoff g (the
-                                    rest took the exact singular branch, rho >= 4.5)   */
+                                    rest took the exact singular branch, rho >= 4.6)   */
   double   ms_keys, ms_sort, ms_tree;                  /* set_particles: a1-a4         */
   double   ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_downward, ms_finalize;
   double   ms_set_total, ms_eval_total;
@@ -218,6 +223,18 @@ fmm_status fmm_rbf_reinit(fmm_ctx* ctx, int64_t n, const float* x, const float* 
  * calls it and broadcasts the bytes to the others, e.g. via torch.distributed;
  * every rank then passes them as fmm_config.nccl_id).  Errors: FMM_E_NCCL. */
 fmm_status fmm_comm_unique_id(void* id);
+
+/* The device's P2P pair arithmetic (a12: k_p2p's pair code) as functions of
+ * rho = r/(sqrt2 sigma_j): g(rho) of Eq. 2 and rho g'(rho) = (4/sqrt pi) rho^3
+ * e^{-rho^2}, recovered from the kernel's f = g/(4 pi r^3) and f'/r =
+ * (rho g' - 3 g)/(4 pi r^5) as ratios to the kernel's own
+ * singular factors (g = f_reg/f_sing, rho g' = 3 g - 3 fp_reg/fp_sing), so the
+ * cutoff approximation of reading Z6 is measured apart from the FP32 1/r^k.
+ * branch 0 = the selection k_p2p applies (exact singular kernel, g = 1 and
+ * rho g' = 0, iff rho >= 4.6), 1 = the regularised branch at every rho.
+ * rho[n] in; g[n], rho_gp[n] out; host or device pointers.  Errors: FMM_E_ARG. */
+fmm_status fmm_eval_pair_kernel(fmm_ctx* ctx, int64_t n, const float* rho, int32_t branch, float* g,
+                                float* rho_gp);
 
 /* The device's FP32 evaluation of the Eq. 2 cutoff g(rho) used by P2P
  * (reading Z6: any approximation with |g - g_exact| <= 2e-7).  rho[n] in,

@@ -84,6 +84,8 @@ def lib():
         L.or_fmm_locals.argtypes = [C.c_void_p, d]
         L.or_fmm_results.argtypes = [C.c_void_p, d, d, d, d]
         L.or_fmm_coverage.argtypes = [C.c_void_p, pi64]
+        L.or_fmm_near_subset.restype = i64
+        L.or_fmm_near_subset.argtypes = [C.c_void_p, i64, pi64, pi64, d, d, pi64]
         _lib = L
     return _lib
 
@@ -263,6 +265,23 @@ class OracleFMM:
         lib().or_fmm_results(self._h, _dp(un), _dp(sn), _dp(uf), _dp(sf))
         return {"u_near": un, "s_near": sn, "u_far": uf, "s_far": sf,
                 "u": un + uf, "s": sn + sf}
+
+    def near_subset(self, leaves):
+        """Near field of the selected target leaves only (sizes where the full
+        evaluation is too slow): returns (caller indices, u_near, s_near, number
+        of P2P entries of those leaves); particles leaf by leaf in sorted order."""
+        leaves = np.ascontiguousarray(leaves, dtype=np.int64)
+        cells = self.cells() if not hasattr(self, "_cells") else self._cells
+        self._cells = cells
+        m = int(cells[leaves, 5].sum()) if len(leaves) else 0
+        pidx = np.zeros(max(m, 1), dtype=np.int64)
+        u = np.zeros((max(m, 1), 3)); s = np.zeros((max(m, 1), 3))
+        ne = C.c_int64(0)
+        got = lib().or_fmm_near_subset(self._h, len(leaves), leaves.ctypes.data_as(C.POINTER(C.c_int64)),
+                                       pidx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(u), _dp(s), C.byref(ne))
+        if got < 0:
+            raise ValueError("near_subset: a selected cell is not a leaf")
+        return pidx[:m], u[:m], s[:m], int(ne.value)
 
     def multipoles(self):
         """Normalised M~ [ncells, 3, P(P+1)/2] complex (reading Z18)."""

@@ -497,17 +497,19 @@ typedef struct { int64_t* v; int64_t len, cap; } stack3;
 /* Alg. 2 Interact (reading Z11).  MAC-first: MAC -> M2L; both
  * leaves -> P2P; else push.  Leaf-first (as printed): both leaves -> P2P;
  * MAC -> M2L; else push.  (The remote branch, only exists with a
- * LET and is not reachable in a single-domain oracle run.) */
-static void interact(or_fmm* f, stack3* st, int64_t A, int64_t B, int img)
+ * LET and is not reachable in a single-domain oracle run.)  The three
+ * destinations are passed in (the f's own lists, or a target subset's). */
+typedef struct { int64_t *p2p, np2p, capp2p, *m2l, nm2l, capm2l; } lists3;
+static void interact_into(or_fmm* f, stack3* st, lists3* out, int64_t A, int64_t B, int img)
 {
   int both_leaves = f->leaf[A] && f->leaf[B];
   if (f->cfg.traversal == 0) {
-    if (mac_accept(f, A, B, img)) push3(&f->m2l, &f->nm2l, &f->capm2l, A, B, img);
-    else if (both_leaves) push3(&f->p2p, &f->np2p, &f->capp2p, A, B, img);
+    if (mac_accept(f, A, B, img)) push3(&out->m2l, &out->nm2l, &out->capm2l, A, B, img);
+    else if (both_leaves) push3(&out->p2p, &out->np2p, &out->capp2p, A, B, img);
     else push3(&st->v, &st->len, &st->cap, A, B, img);
   } else {
-    if (both_leaves) push3(&f->p2p, &f->np2p, &f->capp2p, A, B, img);
-    else if (mac_accept(f, A, B, img)) push3(&f->m2l, &f->nm2l, &f->capm2l, A, B, img);
+    if (both_leaves) push3(&out->p2p, &out->np2p, &out->capp2p, A, B, img);
+    else if (mac_accept(f, A, B, img)) push3(&out->m2l, &out->nm2l, &out->capm2l, A, B, img);
     else push3(&st->v, &st->len, &st->cap, A, B, img);
   }
 }
@@ -522,15 +524,20 @@ static int cmp_triple(const void* pa, const void* pb)
 /* Alg. 1 Evaluate with reading Z10 (equal radius => split B;
  * never split a leaf) and 8c-2 item 7 (seeds: Interact(root, root, img) for
  * the 27 first-layer images when k >= 1). */
-void or_fmm_traverse(or_fmm* f)
+/* The traversal loop over (A, B, img) pairs; keep (may be NULL) restricts the
+ * target side to the flagged cells: a pair whose target cell is not flagged is
+ * dropped, which with keep = "ancestor-or-self of a selected leaf" yields
+ * exactly the full traversal's entries whose target lies on those paths (no
+ * descendant of an unflagged cell is flagged, so no entry for a selected cell
+ * can come from such a pair). */
+static void traverse_into(or_fmm* f, const char* keep, lists3* out)
 {
-  f->np2p = f->nm2l = 0;
   if (f->ncells == 0) return;
   stack3 st = {0, 0, 0};
   if (f->cfg.images > 0) {
-    for (int img = 0; img < 27; ++img) interact(f, &st, 0, 0, img);
+    for (int img = 0; img < 27; ++img) interact_into(f, &st, out, 0, 0, img);
   } else {
-    interact(f, &st, 0, 0, OR_IMG_CENTRE);
+    interact_into(f, &st, out, 0, 0, OR_IMG_CENTRE);
   }
   while (st.len > 0) {
     --st.len;
@@ -538,15 +545,73 @@ void or_fmm_traverse(or_fmm* f)
     int img = (int)st.v[3 * st.len + 2];
     int split_b = f->leaf[A] || (!f->leaf[B] && f->level[B] <= f->level[A]);
     if (split_b) {
-      for (int64_t b = f->child_begin[B]; b < f->child_begin[B] + f->nchild[B]; ++b) interact(f, &st, A, b, img);
+      for (int64_t b = f->child_begin[B]; b < f->child_begin[B] + f->nchild[B]; ++b) interact_into(f, &st, out, A, b, img);
     } else {
-      for (int64_t a = f->child_begin[A]; a < f->child_begin[A] + f->nchild[A]; ++a) interact(f, &st, a, B, img);
+      for (int64_t a = f->child_begin[A]; a < f->child_begin[A] + f->nchild[A]; ++a)
+        if (!keep || keep[a]) interact_into(f, &st, out, a, B, img);
     }
   }
   free(st.v);
   /* canonical order (reading Z20): sort by (target, source, image) */
-  qsort(f->p2p, f->np2p, 3 * sizeof(int64_t), cmp_triple);
-  qsort(f->m2l, f->nm2l, 3 * sizeof(int64_t), cmp_triple);
+  qsort(out->p2p, out->np2p, 3 * sizeof(int64_t), cmp_triple);
+  qsort(out->m2l, out->nm2l, 3 * sizeof(int64_t), cmp_triple);
+}
+
+void or_fmm_traverse(or_fmm* f)
+{
+  lists3 L = {f->p2p, 0, f->capp2p, f->m2l, 0, f->capm2l};
+  traverse_into(f, NULL, &L);
+  f->p2p = L.p2p; f->np2p = L.np2p; f->capp2p = L.capp2p;
+  f->m2l = L.m2l; f->nm2l = L.nm2l; f->capm2l = L.capm2l;
+}
+
+/* Near field (8c-2 item 18: c-1 restricted to P2P list entries) of the
+ * selected target leaves only, for sizes where the full traversal or P2P is
+ * too slow: the traversal above with the target side restricted to the
+ * ancestors-or-self of the selected leaves, then c-1 over each selected
+ * leaf's P2P entries in canonical order (the same arithmetic and summation
+ * order as or_fmm_evaluate's P2P).  For each selected leaf in the given order,
+ * its particles (sorted order) are written to pidx (caller index), u, s.
+ * Returns the number of particles written, or -1 if a cell is not a leaf. */
+int64_t or_fmm_near_subset(or_fmm* f, int64_t nsel, const int64_t* leaves, int64_t* pidx, double* u, double* s,
+                           int64_t* np2p_out)
+{
+  char* keep = calloc(f->ncells ? f->ncells : 1, 1);
+  for (int64_t k = 0; k < nsel; ++k) {
+    int64_t c = leaves[k];
+    if (c < 0 || c >= f->ncells || !f->leaf[c]) { free(keep); return -1; }
+    for (; c >= 0; c = f->parent[c]) keep[c] = 1;
+  }
+  lists3 L = {NULL, 0, 0, NULL, 0, 0};
+  if (nsel > 0) traverse_into(f, keep, &L);
+  int64_t* seg = calloc(f->ncells + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < L.np2p; ++e) seg[L.p2p[3 * e] + 1]++;
+  for (int64_t c = 0; c < f->ncells; ++c) seg[c + 1] += seg[c];
+  int64_t* first = malloc(sizeof(int64_t) * (nsel ? nsel : 1));
+  int64_t m = 0;
+  for (int64_t k = 0; k < nsel; ++k) { first[k] = m; m += f->count[leaves[k]]; }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t k = 0; k < nsel; ++k) {
+    int64_t t = leaves[k];
+    for (int64_t i = f->begin[t]; i < f->begin[t] + f->count[t]; ++i) {
+      double ui[3] = {0, 0, 0}, si[3] = {0, 0, 0};
+      for (int64_t e = seg[t]; e < seg[t + 1]; ++e) {
+        int64_t sc = L.p2p[3 * e + 1];
+        int v[3]; img_shift((int)L.p2p[3 * e + 2], v);
+        for (int64_t j = f->begin[sc]; j < f->begin[sc] + f->count[sc]; ++j) {
+          double r[3];
+          for (int d = 0; d < 3; ++d) r[d] = f->xs[3 * i + d] - f->xs[3 * j + d] - v[d] * f->L;
+          pair_kernel(r, &f->as[3 * j], f->ss[j], &f->as[3 * i], ui, si);
+        }
+      }
+      int64_t o = first[k] + (i - f->begin[t]);
+      pidx[o] = f->perm[i];
+      for (int d = 0; d < 3; ++d) { u[3 * o + d] = ui[d]; s[3 * o + d] = si[d]; }
+    }
+  }
+  if (np2p_out) *np2p_out = L.np2p;
+  free(first); free(seg); free(keep); free(L.p2p); free(L.m2l);
+  return m;
 }
 
 /* segment boundaries of a target-sorted list */

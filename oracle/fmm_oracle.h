@@ -92,6 +92,13 @@ void    or_fmm_multipoles(const or_fmm* f, double* out);
 void    or_fmm_locals(const or_fmm* f, double* out);
 /* results in caller order, [n][3] each */
 void    or_fmm_results(const or_fmm* f, double* u_near, double* s_near, double* u_far, double* s_far);
+/* near field of the selected target leaves only (8c-2 item 18 restricted to
+ * their P2P entries; the traversal's target side restricted to their
+ * ancestors): for each leaves[k] in order, its particles in sorted order ->
+ * pidx (caller index), u[.][3], s[.][3]; *np2p = the leaves' P2P entries.
+ * Returns the particle count written, -1 if a listed cell is not a leaf. */
+int64_t or_fmm_near_subset(or_fmm* f, int64_t nsel, const int64_t* leaves, int64_t* pidx, double* u, double* s,
+                           int64_t* np2p);
 /* traversal completeness: per particle (caller order) number of source
  * particles covered by P2P + M2L + periodic far field. */
 void    or_fmm_coverage(const or_fmm* f, int64_t* cover);

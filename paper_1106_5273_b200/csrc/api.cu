@@ -180,6 +180,12 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   m2l_pass(c);
   periodic_far_pass(c);
   FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
+  // no owned leaf (a rank without whole leaves): nothing below writes the
+  // near/far buffers, so they are defined as zero here
+  if (c.nleaves == 0) {
+    for (float* b : {c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p})
+      FMM_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, st));
+  }
   // a12 P2P
   p2p_pass(c, c.u_near.p, c.s_near.p);
   FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));
@@ -288,7 +294,10 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     if (cfg->stream) {
       c.stream = (cudaStream_t)cfg->stream;
     } else {
-      FMM_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      // blocking: ordered with the legacy default stream, so caller work queued
+      // there (e.g. torch's default stream) completes before the library reads
+      // its inputs, and the library's writes precede later default-stream work
+      FMM_CUDA(cudaStreamCreate(&c.stream));
       c.own_stream = true;
     }
     for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
@@ -502,6 +511,29 @@ FMM_API fmm_status fmm_eval_cutoff(fmm_ctx* h, int64_t n, const float* rho, floa
     FMM_CUDA(cudaMemcpyAsync(c.stage_u.p, rho, sizeof(float) * n, cudaMemcpyDefault, c.stream));
     eval_cutoff(c, c.stage_u.p, n, c.stage_ds.p);
     FMM_CUDA(cudaMemcpyAsync(g, c.stage_ds.p, sizeof(float) * n, cudaMemcpyDefault, c.stream));
+    FMM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+FMM_API fmm_status fmm_eval_pair_kernel(fmm_ctx* h, int64_t n, const float* rho, int32_t branch, float* g,
+                                        float* rho_gp) {
+  if (!h) return FMM_E_ARG;
+  Ctx& c = h->c;
+  if (c.poisoned) return FMM_E_STATE;
+  return guard(&c, [&] {
+    if (n < 0 || (n > 0 && (!rho || !g || !rho_gp)) || branch < 0 || branch > 1)
+      throw FmmError(FMM_E_ARG, "bad arguments");
+    if (n == 0) return;
+    FMM_CUDA(cudaSetDevice(c.cfg.device));
+    c.stage_u.reserve(3 * n);
+    c.stage_ds.reserve(3 * n);
+    float* dr = c.stage_u.p;
+    float* dg = c.stage_ds.p;
+    float* dp = c.stage_ds.p + n;
+    FMM_CUDA(cudaMemcpyAsync(dr, rho, sizeof(float) * n, cudaMemcpyDefault, c.stream));
+    eval_pair_kernel(c, dr, n, branch, dg, dp);
+    FMM_CUDA(cudaMemcpyAsync(g, dg, sizeof(float) * n, cudaMemcpyDefault, c.stream));
+    FMM_CUDA(cudaMemcpyAsync(rho_gp, dp, sizeof(float) * n, cudaMemcpyDefault, c.stream));
     FMM_CUDA(cudaStreamSynchronize(c.stream));
   });
 }

@@ -164,6 +164,7 @@ void fill_f32(Ctx& c, float* p, int64_t n, float v);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near);
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g);
+void eval_pair_kernel(Ctx& c, const float* rho, int64_t n, int branch, float* g, float* rgp);
 void gauss_pass(Ctx& c, const float4* q, double* out);
 void rbf_reinit_impl(Ctx& c, int64_t n, const float* x, const float* alpha, const float* sigma, int64_t m,
                      const float* y, float sigma0, double tol, int maxit, float* beta_out, int* iters, double* resid);

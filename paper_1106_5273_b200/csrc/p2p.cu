@@ -25,10 +25,12 @@
 // the parity tests through fmm_eval_cutoff).  The pair arithmetic of the two
 // targets of a lane is packed into FP32x2 (FFMA2) with the source operands
 // broadcast, halving the issue slots per pair.  Sources whose every pair
-// with the targets has rho >= 4.5 (distance from the source to the tight box
-// of the targets >= 4.5 sqrt2 sigma_j, tested once per source while staging) are
+// with the targets has rho >= 4.6 (distance from the source to the tight box
+// of the targets >= 4.6 sqrt2 sigma_j, tested once per source while staging) are
 // compacted to the front of the tile and take the exact singular branch:
-// there 1 - g < 1e-8, so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
+// there 1 - g < 4e-9 and rho g' = (4/sqrt pi) rho^3 e^{-rho^2} < 1.5e-7 (both
+// within reading Z6's 2e-7), so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
+// fmm_eval_pair_kernel exports both branches' g and rho g' for the Z6 test.
 #include "ctx.cuh"
 
 namespace fmmb {
@@ -37,6 +39,7 @@ namespace {
 
 constexpr int TP = 64;           // targets per block pass and sources per tile
 constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
+constexpr float kFarRho2 = 4.6f * 4.6f;   // rho^2 at and beyond which the singular branch is exact to Z6
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
@@ -135,7 +138,7 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
   const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
   float2 inv;
   if (NEAR) inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
-  else inv = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));      // rho >= 4.5: r > 0
+  else inv = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));      // rho >= 4.6: r > 0
   const float2 inv2 = __fmul2_rn(inv, inv);
   const float2 inv3 = __fmul2_rn(inv2, inv);
   float2 f, fp3;
@@ -306,8 +309,9 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
         // stage the tile, far sources first: a source is "far" when it is
-        // >= 4.5 sqrt2 sigma_j from the whole target leaf cube, so every pair
-        // it forms has rho >= 4.5 (then 1 - g < 1e-8: the exact singular branch)
+        // >= 4.6 sqrt2 sigma_j from the whole target leaf cube, so every pair
+        // it forms has rho >= 4.6 (then 1 - g < 4e-9 and rho g' < 1.5e-7: the
+        // exact singular branch, reading Z6)
         float4 qv[2], av[2], wv[2], cv[2];
         bool fj[2], vj[2];
 #pragma unroll
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
             cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx - bc[0]) - bh[0]), gy = fmaxf(0.f, fabsf(qy - bc[1]) - bh[1]),
                         gz = fmaxf(0.f, fabsf(qz - bc[2]) - bh[2]);
-            fj[h] = (gx * gx + gy * gy + gz * gz) * w >= 20.25f * 1.0001f;
+            fj[h] = (gx * gx + gy * gy + gz * gz) * w >= kFarRho2 * 1.0001f;
           }
         }
         const unsigned lt = (1u << lane) - 1u;
@@ -391,7 +395,55 @@ __global__ void k_eval_cutoff(const float* __restrict__ rho, int64_t n, float* _
   }
 }
 
+// The pair arithmetic of k_p2p (pair2, both branches) on one source at the
+// origin with sqrt2 sigma = 1 and targets at r = rho on the x axis (two rho per
+// thread, as the lane pairs of k_p2p), alpha_j = alpha_i = x-hat: fa0 = f and
+// qa0 = r fp/(-3).  The regularised factors are reported relative to the
+// singular ones of the same code (same rsqrt of the same r^2), which isolates
+// the cutoff approximation (reading Z6) from the FP32 evaluation of 1/r^k:
+//   g = f_reg / f_sing,   rho g' = 3 g - 3 fp_reg / fp_sing
+// (f = g/r^3, f'/r = (rho g' - 3 g)/r^5).  branch 0 = the selection
+// k_p2p applies (singular, i.e. g = 1 and rho g' = 0, iff rho^2 >= kFarRho2),
+// branch 1 = the regularised branch at every rho.
+__global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch, float* __restrict__ g,
+                            float* __restrict__ rgp) {
+  // no early exit: pair2<true> votes across the whole warp
+  const int64_t i0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const float r0 = i0 < n ? rho[i0] : 1.f, r1 = i0 + 1 < n ? rho[i0 + 1] : 1.f;
+  const float w = 0.5f;                                     // 1/(2 sigma^2) with sqrt2 sigma = 1
+  const float4 q = make_float4(0.f, 0.f, 0.f, -1.4426950408889634f * w);
+  const float aw = sqrtf(w);
+  const float4 a = make_float4(1.f, 0.f, 0.f, aw);
+  const float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 cv = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
+  const float2 X0 = make_float2(r0, r1), X1 = make_float2(0.f, 0.f), X2 = make_float2(0.f, 0.f);
+  const float2 B0 = make_float2(1.f, 1.f), B1 = make_float2(0.f, 0.f), B2 = make_float2(0.f, 0.f);
+  Acc2 An, Af;
+  zero(An);
+  zero(Af);
+  pair2<true>(An, X0, X1, X2, B0, B1, B2, q, a, wv, cv);
+  pair2<false>(Af, X0, X1, X2, B0, B1, B2, q, a, wv, a);
+  const float rr[2] = {r0, r1};
+  const float fn[2] = {An.fa0.x, An.fa0.y}, ff[2] = {Af.fa0.x, Af.fa0.y};
+  const float pn[2] = {An.qa0.x, An.qa0.y}, pf[2] = {Af.qa0.x, Af.qa0.y};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t i = i0 + h;
+    if (i >= n) continue;
+    const bool sing = branch == 0 && rr[h] * rr[h] >= kFarRho2;
+    if (rr[h] <= 0.f) { g[i] = 0.f; rgp[i] = 0.f; continue; }       // r = 0 contributes nothing (Z7)
+    const double gd = sing ? 1.0 : (double)fn[h] / (double)ff[h];
+    const double pd = sing ? 1.0 : (double)pn[h] / (double)pf[h];
+    g[i] = (float)gd;
+    rgp[i] = (float)(3.0 * gd - 3.0 * pd);
+  }
+}
+
 }  // namespace
+
+void eval_pair_kernel(Ctx& c, const float* rho, int64_t n, int branch, float* g, float* rgp) {
+  FMM_LAUNCH(c, k_eval_pair, nblocks((n + 1) / 2, 256), 256, 0, rho, n, branch, g, rgp);
+}
 
 void p2p_pass(Ctx& c, float* u_near, float* s_near) {
   if (c.nleaves == 0) return;

@@ -81,6 +81,7 @@ def lib():
         L.fmm_get_lists.argtypes = [vp, vp, vp]
         L.fmm_get_expansions.argtypes = [vp, vp, vp]
         L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
+        L.fmm_eval_pair_kernel.argtypes = [vp, i64, vp, C.c_int32, vp, vp]
         L.fmm_comm_unique_id.argtypes = [vp]
         L.fmm_step.argtypes = [vp, i64, vp, vp, vp, C.c_double, C.c_double]
         L.fmm_evaluate_targets.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
@@ -88,21 +89,30 @@ def lib():
                                      C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         for nm in ("fmm_create", "fmm_set_particles", "fmm_evaluate", "fmm_evaluate_parts", "fmm_destroy",
                    "fmm_get_stats", "fmm_get_sizes", "fmm_get_box", "fmm_get_keys", "fmm_get_cells",
-                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_comm_unique_id", "fmm_step",
+                   "fmm_get_lists", "fmm_get_expansions", "fmm_eval_cutoff", "fmm_eval_pair_kernel",
+                   "fmm_comm_unique_id", "fmm_step",
                    "fmm_evaluate_targets", "fmm_rbf_reinit"):
             getattr(L, nm).restype = C.c_int
         _lib = L
     return _lib
 
 
-def _ptr(a):
+def _ptr(a, numel=None, device=None):
+    """Raw pointer of a float32 array; numel: required element count; device:
+    the context's CUDA ordinal (a CUDA tensor on another GPU is rejected)."""
     if a is None:
+        if numel:
+            raise ValueError("array required")
         return None
+    if numel is not None and int(np.prod(a.shape)) != int(numel):
+        raise ValueError("array has %d elements, expected %d" % (int(np.prod(a.shape)), int(numel)))
     if hasattr(a, "data_ptr"):          # torch tensor
         if str(a.dtype) != "torch.float32":
             raise TypeError("float32 tensor required")
         if not a.is_contiguous():
             raise ValueError("contiguous tensor required")
+        if device is not None and a.is_cuda and a.device.index != int(device):
+            raise ValueError("tensor on cuda:%d, context on cuda:%d" % (a.device.index, int(device)))
         return C.c_void_p(a.data_ptr())
     if isinstance(a, np.ndarray):
         if a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
@@ -141,16 +151,20 @@ def fmm_create(cfg: fmm_config):
     return h
 
 
-def fmm_set_particles(ctx, n, x, alpha, sigma):
-    _check(ctx, lib().fmm_set_particles(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma)))
+def fmm_set_particles(ctx, n, x, alpha, sigma, device=None):
+    n = int(n)
+    _check(ctx, lib().fmm_set_particles(ctx, n, _ptr(x, 3 * n, device), _ptr(alpha, 3 * n, device),
+                                        _ptr(sigma, n, device)))
 
 
-def fmm_evaluate(ctx, u, dalpha_dt):
-    _check(ctx, lib().fmm_evaluate(ctx, _ptr(u), _ptr(dalpha_dt)))
+def fmm_evaluate(ctx, u, dalpha_dt, n=None, device=None):
+    m = None if n is None else 3 * int(n)
+    _check(ctx, lib().fmm_evaluate(ctx, _ptr(u, m, device), _ptr(dalpha_dt, m, device)))
 
 
-def fmm_evaluate_parts(ctx, parts, u, dalpha_dt):
-    _check(ctx, lib().fmm_evaluate_parts(ctx, int(parts), _ptr(u), _ptr(dalpha_dt)))
+def fmm_evaluate_parts(ctx, parts, u, dalpha_dt, n=None, device=None):
+    m = None if n is None else 3 * int(n)
+    _check(ctx, lib().fmm_evaluate_parts(ctx, int(parts), _ptr(u, m, device), _ptr(dalpha_dt, m, device)))
 
 
 def fmm_destroy(ctx):
@@ -211,20 +225,25 @@ def fmm_get_expansions(ctx, order):
     return (M[..., 0] + 1j * M[..., 1]).astype(np.complex128), (L[..., 0] + 1j * L[..., 1]).astype(np.complex128)
 
 
-def fmm_step(ctx, n, x, alpha, sigma, dt, nu):
-    _check(ctx, lib().fmm_step(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), float(dt), float(nu)))
+def fmm_step(ctx, n, x, alpha, sigma, dt, nu, device=None):
+    n = int(n)
+    _check(ctx, lib().fmm_step(ctx, n, _ptr(x, 3 * n, device), _ptr(alpha, 3 * n, device), _ptr(sigma, n, device),
+                               float(dt), float(nu)))
 
 
-def fmm_evaluate_targets(ctx, n, x, alpha, sigma, nt, y, u):
-    _check(ctx, lib().fmm_evaluate_targets(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), int(nt), _ptr(y),
-                                           _ptr(u)))
+def fmm_evaluate_targets(ctx, n, x, alpha, sigma, nt, y, u, device=None):
+    n, nt = int(n), int(nt)
+    _check(ctx, lib().fmm_evaluate_targets(ctx, n, _ptr(x, 3 * n, device), _ptr(alpha, 3 * n, device),
+                                           _ptr(sigma, n, device), nt, _ptr(y, 3 * nt, device),
+                                           _ptr(u, 3 * nt, device)))
 
 
 def fmm_rbf_reinit(ctx, n, x, alpha, sigma, m, y, sigma0, tol, maxit, beta):
     """NEXT-4: returns (iterations, relative residual); FMMError(FMM_E_NOCONV) if maxit is reached."""
     it, res = C.c_int32(0), C.c_double(0.0)
-    st = lib().fmm_rbf_reinit(ctx, int(n), _ptr(x), _ptr(alpha), _ptr(sigma), int(m), _ptr(y), float(sigma0),
-                              float(tol), int(maxit), _ptr(beta), C.byref(it), C.byref(res))
+    n, m = int(n), int(m)
+    st = lib().fmm_rbf_reinit(ctx, n, _ptr(x, 3 * n), _ptr(alpha, 3 * n), _ptr(sigma, n), m, _ptr(y, 3 * m),
+                              float(sigma0), float(tol), int(maxit), _ptr(beta, 3 * m), C.byref(it), C.byref(res))
     if st == FMM_E_NOCONV:
         raise FMMError(st, "%d iterations, relative residual %.3e > tol %.1e" % (it.value, res.value, tol))
     _check(ctx, st)
@@ -240,7 +259,14 @@ def fmm_comm_unique_id() -> bytes:
 
 
 def fmm_eval_cutoff(ctx, rho, g):
-    _check(ctx, lib().fmm_eval_cutoff(ctx, int(rho.shape[0]), _ptr(rho), _ptr(g)))
+    n = int(rho.shape[0])
+    _check(ctx, lib().fmm_eval_cutoff(ctx, n, _ptr(rho, n), _ptr(g, n)))
+
+
+def fmm_eval_pair_kernel(ctx, rho, g, rho_gp, branch=0):
+    """g(rho) and rho g'(rho) as the device P2P pair code evaluates them (reading Z6)."""
+    n = int(rho.shape[0])
+    _check(ctx, lib().fmm_eval_pair_kernel(ctx, n, _ptr(rho, n), int(branch), _ptr(g, n), _ptr(rho_gp, n)))
 
 
 class FMM:
@@ -257,20 +283,21 @@ class FMM:
         self.n = 0
 
     def set_particles(self, x, alpha, sigma):
-        self.n = int(x.shape[0])
-        fmm_set_particles(self.ctx, self.n, x, alpha, sigma)
+        n = int(x.shape[0])
+        fmm_set_particles(self.ctx, n, x, alpha, sigma, device=self.cfg.device)
+        self.n = n
 
     def evaluate(self, u, dalpha_dt, parts=3):
-        fmm_evaluate_parts(self.ctx, parts, u, dalpha_dt)
+        fmm_evaluate_parts(self.ctx, parts, u, dalpha_dt, n=self.n, device=self.cfg.device)
 
     def step(self, x, alpha, sigma, dt, nu=0.0):
         """One midpoint-RK2 vortex step (NEXT-1); overwrites x, alpha, sigma."""
-        fmm_step(self.ctx, x.shape[0], x, alpha, sigma, dt, nu)
+        fmm_step(self.ctx, x.shape[0], x, alpha, sigma, dt, nu, device=self.cfg.device)
         self.n = int(x.shape[0])
 
     def evaluate_targets(self, x, alpha, sigma, y, u):
         """Velocity at strength-free targets y (NEXT-2); the context then holds the union."""
-        fmm_evaluate_targets(self.ctx, x.shape[0], x, alpha, sigma, y.shape[0], y, u)
+        fmm_evaluate_targets(self.ctx, x.shape[0], x, alpha, sigma, y.shape[0], y, u, device=self.cfg.device)
         self.n = int(x.shape[0] + y.shape[0])
 
     def rbf_reinit(self, x, alpha, sigma, y, sigma0, beta, tol=1e-6, maxit=200):
