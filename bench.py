@@ -61,7 +61,11 @@ def parse():
                     help="N > 1 with --mode strong: octant = each rank passes its Morton-octant block; balanced = "
                          "each rank passes a random 1/N subset and the library redistributes it every step "
                          "(cfg.partition = 1: equal-count Morton ranges cut at leaf boundaries, NEXT-3)")
-    ap.add_argument("--cpu-sample", type=int, default=32, help="oracle sample: TG n^3 lattice")
+    ap.add_argument("--workload", choices=["lattice", "jitter", "advected"], default="lattice",
+                    help="N = 1 stress variants of C3 (VERDICT r01): jitter = the lattice jittered by +-h "
+                         "(seed 5273); advected = the lattice after one fmm_step (midpoint RK2, dt = 2h, "
+                         "max displacement ~2h): leaves gain and lose particles, the tree turns adaptive")
+    ap.add_argument("--cpu-fmm-sample", type=int, default=64, help="cpu_baseline: oracle FMM on TG n^3 (C2 = 64)")
     ap.add_argument("--ref-sample", type=int, default=24, help="--impl reference sample: TG n^3 lattice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -142,15 +146,46 @@ def oracle_step(n, order, images, theta, ncrit):
 
 
 def cpu_baseline(args, theta):
+    """SURVEY 8(d) CPU plan, on this host's cores (OpenMP, double): the oracle
+    FMM timed on C1 and C2 (the metric's value is the C2 run, 174 x P2P pairs /
+    s), and the direct sum's pair rate measured on a seeded target sample of
+    C2 (free space), from which the full C1 periodic, C2 free-space and C3
+    direct sums are extrapolated (labelled so; one pair = one evaluation of
+    Eq. 1 + Eq. 3 per source image)."""
     import oracle
+    import synth
     oracle.build()
     cores = os.cpu_count()
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    dt, pairs = oracle_step(args.cpu_sample, args.order, args.images, theta, args.ncrit)
-    return {"value": FLOPS_PER_PAIR * pairs / dt / 1e12, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
-            "kind": "oracle",
-            "sample": "oracle FMM step (double, OpenMP) on Taylor-Green %d^3 = %d particles, same p/theta/ncrit/k; "
-                      "%.2f s, %d P2P pairs" % (args.cpu_sample, args.cpu_sample ** 3, dt, pairs)}
+    out = {"unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]), "nproc": cores, "kind": "oracle"}
+    # direct-sum pair rate: 4 x cores seeded targets of C2 against all 262,144 sources (free space)
+    x, a, s = synth.taylor_green(64)
+    nt = 4 * cores
+    idx = np.random.default_rng(1106).choice(len(x), nt, replace=False)
+    t0 = time.perf_counter()
+    oracle.direct(x[idx], a[idx], x, a, s, images=0)
+    dt = time.perf_counter() - t0
+    rate = nt * len(x) / dt
+    n1, n2, n3 = 16 ** 3, 64 ** 3, 256 ** 3
+    img3 = 27 ** 3
+    out["direct_pairs_per_s"] = rate
+    out["direct_sample"] = "C2 free space, %d seeded targets x %d sources in %.2f s" % (nt, len(x), dt)
+    out["c1_periodic_direct_s_extrapolated"] = n1 * n1 * img3 / rate
+    out["c2_free_direct_s_extrapolated"] = n2 * n2 / rate
+    out["c3_free_direct_s_extrapolated"] = n3 * n3 / rate
+    out["c3_periodic_direct_s_extrapolated"] = n3 * n3 * img3 / rate
+    fmm = {}
+    for name, nside in (("c1", 16), ("c2", args.cpu_fmm_sample)):
+        dtf, pairs = oracle_step(nside, args.order, args.images, theta, args.ncrit)
+        fmm[name] = (dtf, pairs)
+        out["%s_fmm_s" % name] = dtf
+    dtf, pairs = fmm["c2"]
+    out["value"] = FLOPS_PER_PAIR * pairs / dtf / 1e12
+    out["sample"] = ("oracle FMM step (double, OpenMP, %d threads) on Taylor-Green %d^3 = %d particles (C2 at 64), "
+                     "same p/theta/ncrit/k: %.2f s, %d P2P pairs; C1 FMM %.2f s; direct sums extrapolated from "
+                     "the measured pair rate" % (out["cores"], args.cpu_fmm_sample, args.cpu_fmm_sample ** 3, dtf,
+                                                 pairs, fmm["c1"][0]))
+    return out
 
 
 def run_reference(args):
@@ -225,8 +260,12 @@ def main():
     if balanced:
         full = synth.taylor_green(args.side)
         x, a, s = (v[synth.scatter_to_ranks(len(full[0]), world, rank)] for v in full)
+    elif world == 1 and args.workload == "jitter":
+        x, a, s = synth.jittered_lattice(args.side, amp=1.0)
     else:
         x, a, s = gen(args.side, world, rank)
+    if args.workload != "lattice" and world > 1:
+        raise SystemExit("--workload variants are single-GPU")
     n = len(x)
     stream = torch.cuda.Stream()
     nccl_id = None
@@ -241,6 +280,13 @@ def main():
         xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
         ud = torch.empty((n, 3), device="cuda")
         dd = torch.empty((n, 3), device="cuda")
+        if args.workload == "advected":
+            # the state after one vortex-method step (NEXT-1): particles leave the lattice,
+            # leaves gain/lose particles and the tree turns adaptive (the paper's lattice
+            # only returns to uniform at reinitialisation)
+            f.step(xd, ad, sd, 2.0 * float(s[0]), 0.0)
+        torch.cuda.synchronize()
+        x, a, s = (t.cpu().numpy() for t in (xd, ad, sd))
 
     def step():
         f.set_particles(xd, ad, sd)
@@ -267,25 +313,39 @@ def main():
     clk = ClockSampler(gpu_index)
     clk.start()
     time.sleep(0.3)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    stats = []
+    # timed region: K steps, one CUDA event between consecutive steps (library stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             step()
-            stats.append(f.stats())
-        e1.record(stream)
+            evs[i + 1].record(stream)
     barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1) / args.steps
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms_mean = evs[0].elapsed_time(evs[-1]) / args.steps
+    ms = statistics.median(per_step)            # median of the timed steps
+    # per-phase CUDA-event times and counters: separate untimed steps (no host work in the timed region)
+    stats = []
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step()
+            stats.append(f.stats())
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
 
     pairs = stats[-1]["p2p_pairs"]
-    launches = sum(st["launches"] for st in stats)
-    cub_calls = sum(st["cub_calls"] for st in stats)
-    phase = {k: statistics.mean(st[k] for st in stats) for k in
-             ("ms_keys", "ms_sort", "ms_tree", "ms_upward", "ms_traverse", "ms_m2l", "ms_p2p", "ms_downward",
-              "ms_finalize", "ms_set_total", "ms_eval_total")}
+    launches = stats[-1]["launches"] * args.steps
+    cub_calls = stats[-1]["cub_calls"] * args.steps
+    phase = {k: statistics.median(st[k] for st in stats) for k in
+             ("ms_keys", "ms_sort", "ms_tree", "ms_upward", "ms_traverse", "ms_m2l", "ms_m2l_tc", "ms_m2l_reg",
+              "ms_p2p", "ms_downward", "ms_finalize", "ms_set_total", "ms_eval_total")}
+    m2l_split = {k: stats[-1][k] for k in ("m2l_list", "m2l_tc_list", "m2l_reg_list")}
+    m2l_split["tc_fraction"] = m2l_split["m2l_tc_list"] / max(1, m2l_split["m2l_list"])
+    m2l_split["reg_kernel_tflops_algorithmic"] = (29040.0 * m2l_split["m2l_reg_list"] / (phase["ms_m2l_reg"] * 1e-3) / 1e12
+                                                  if phase["ms_m2l_reg"] > 0 else None)
+    m2l_split["reg_kernel_frac_fp32_peak"] = (m2l_split["reg_kernel_tflops_algorithmic"] / FP32_PEAK_TFLOPS
+                                              if m2l_split["reg_kernel_tflops_algorithmic"] else None)
 
     # e2e through the C ABI from pinned host buffers
     e2e = None
@@ -312,12 +372,13 @@ def main():
                "d2h_bytes_per_step": int(uh.numel() * 4 + dh.numel() * 4), "pairs": pairs}
 
     # aggregate over ranks: max time, summed work
-    t = torch.tensor([ms, e2e["ms_per_step"] if e2e else 0.0, phase["ms_p2p"]], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, e2e["ms_per_step"] if e2e else 0.0, phase["ms_p2p"], ms_mean], dtype=torch.float64,
+                     device="cuda")
     w = torch.tensor([float(pairs), float(n)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(w, op=dist.ReduceOp.SUM)
-    ms_max, ms_e2e_max, p2p_ms_max = t.tolist()
+    ms_max, ms_e2e_max, p2p_ms_max, ms_mean_max = t.tolist()
     tot_pairs, tot_n = w.tolist()
     value = FLOPS_PER_PAIR * tot_pairs / (ms_max * 1e-3) / 1e12
 
@@ -325,7 +386,7 @@ def main():
         traffic, prof = load_profile_traffic()
         from tools.sass_flops import p2p_flops_per_pair, sass_digest
         fpp = p2p_flops_per_pair(P.fmm.LIB_PATH)
-        near = statistics.mean(st["p2p_near_pairs"] for st in stats)
+        near = stats[-1]["p2p_near_pairs"]
         hw_flops = near * fpp.get("near", 0.0) + (pairs - near) * fpp.get("far", 0.0)
         flops_src = "static SASS count (tools/sass_flops.py)"
         # prefer the ncu-counted flops of this exact build on this exact workload
@@ -361,11 +422,18 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "s_per_step": ms_max / 1e3,
+            "timing": {"statistic": "median of the %d timed steps (CUDA events between steps, library stream; "
+                                    "max over ranks)" % args.steps,
+                       "ms_per_step_mean": ms_mean_max, "ms_steps_rank0": per_step},
             "higher_is_better": True, "scaling": "strong" if (world > 1 and args.mode == "strong") else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic Taylor-Green lattice (reading Z26), generated on host, resident in HBM",
-            "config": {"workload": ("C3: Taylor-Green %d^3 = %d particles per GPU, periodic k=%d, p=%d, theta=%s, "
-                                    "ncrit=%d" % (args.side, n, args.images, args.order, args.theta, args.ncrit))
+            "config": {"workload": ("C3: Taylor-Green %d^3 = %d particles per GPU%s, periodic k=%d, p=%d, theta=%s, "
+                                    "ncrit=%d" % (args.side, n, {"lattice": "", "jitter": " (stress: lattice jittered "
+                                                                 "by +-h/4, seed 5273)",
+                                                                 "advected": " (stress: after one fmm_step, midpoint "
+                                                                 "RK2 with dt = h/2)"}[args.workload],
+                                                  args.images, args.order, args.theta, args.ncrit))
                        if world == 1 else
                        ("C5 weak scaling: %s tiles of the 2pi Taylor-Green cube, one %d^3 = %d-particle tile per "
                         "GPU, periodic k=%d, p=%d, theta=%s, ncrit=%d (reading Z27)" %
@@ -392,6 +460,7 @@ def main():
             "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
             "particles_per_s": tot_n / (ms_max * 1e-3),
             "phases_ms": phase,
+            "m2l_split": m2l_split,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": None if not e2e else {

@@ -79,28 +79,31 @@ typedef struct {
   int32_t  traversal;            /* 0 = MAC-first (default), 1 = leaf-first (Z11)      */
   int32_t  device;               /* CUDA ordinal                                       */
   void*    stream;               /* cudaStream_t for all work; NULL = library-owned    */
-  int32_t  rank, nranks;         /* partition = 0: nranks in {1,2,4,8} and rank r owns the
-                                    particles whose Morton keys lie in top octants
-                                    [8r/P, 8(r+1)/P) (each rank passes only those,
-                                    else FMM_E_ARG); partition = 1: 1 <= nranks <= 8   */
+  int32_t  rank, nranks;         /* 1 <= nranks <= 8 (one NVLink node), one rank per GPU;
+                                    nranks > 1 needs images >= 1 (see partition)       */
   const void* nccl_id;           /* 128-byte ncclUniqueId when nranks > 1 (all ranks
                                     pass the same id, e.g. broadcast by torch.distributed) */
   int32_t  tiles[3];             /* periodic domain of tiles[d] cubes of side box_len per
                                     axis (reading Z27, weak scaling); tiles[d] in {1, 2},
-                                    default (1,1,1).  With tiles != (1,1,1) rank r owns
-                                    tile/top octant r and nranks = tiles product       */
+                                    default (1,1,1).  Tile t is top-level octant t of the
+                                    root cube (x fastest); any rank may hold any part  */
   int32_t  m2l_path;             /* 0 (default): tensor-core M2L (tcgen05, 3xTF32) on the
                                     levels whose cells share one offset set, register
                                     kernel elsewhere; 1: register (CUDA-core) kernel only */
-  int32_t  partition;            /* multi-GPU ownership (tiles == (1,1,1) only):
-                                    0 (default): the caller's octant blocks (above);
-                                    1: balanced -- every rank passes ANY of the particles;
-                                    set_particles sorts all keys globally, cuts the Morton
-                                    curve into nranks equal-count ranges moved to the
-                                    nearest leaf boundary (load balancing),
-                                    redistributes the particles to their owners (NCCL)
-                                    and evaluate returns every rank its own particles'
-                                    results in its caller order                          */
+  int32_t  partition;            /* multi-GPU domain decomposition (a14, NEXT-3):
+                                    0 (default): every rank's targets are the particles it
+                                    passes (e.g. its octant blocks or tiles);
+                                    1: ORB recursive multisection at every
+                                    set_particles -- the particles (any distribution, any
+                                    subset per rank) are split at the nth element of x,
+                                    y, z, ... (distributed radix select, NCCL all-reduce of
+                                    histograms) into nranks equal-count boxes and moved to
+                                    their owners; evaluate returns every rank its own
+                                    particles' results in its caller order;
+                                    2: as 1, with the cuts of the first set_particles kept
+                                    ("the partitioning is performed only once").
+                                    Every rank then builds the octree of its own particles
+                                    and exchanges local essential trees      */
 } fmm_config;
 
 /* Per-phase device times of the last set_particles / evaluate (CUDA events on
@@ -127,6 +130,14 @@ typedef struct {
   int64_t  m2l_tc_list;                     /* M2L entries evaluated on the tensor cores    */
   int64_t  own_begin, own_count;            /* global sorted positions this rank owns        */
   int64_t  redist_bytes;                    /* partition = 1: particle bytes sent by set_particles */
+  int64_t  m2l_reg_list;                    /* M2L entries evaluated by the register (CUDA-core) kernel */
+  double   ms_m2l_tc, ms_m2l_reg;           /* M2L phase split: tensor-core kernel (+ its pack), register kernel */
+  double   ms_let_exposed;                  /* LET wait of the main stream after the local near field */
+  int64_t  let_fallback;                    /* pairs resolved by Alg. 2's remote branch (M2L with the
+                                               smallest cell received): 0 = complete LET */
+  int64_t  nranks;
+  int64_t  ncells_local;                    /* cells of this rank's own tree (ids [0, ncells_local));
+                                               the rest of ncells are the peers' LETs          */
 } fmm_stats;
 
 /* Fill cfg with the defaults listed above. */

@@ -31,34 +31,6 @@ __global__ void k_finalize(const uint32_t* __restrict__ idx, int64_t n, int64_t 
   }
 }
 
-// balanced partition: owned results in receive order (6 floats: u, s), sent back
-// to the ranks the particles came from; there they land in the caller's order
-__global__ void k_ret_pack(const int* __restrict__ gp, int64_t m, int parts, const float* __restrict__ un,
-                           const float* __restrict__ sn, const float* __restrict__ uf, const float* __restrict__ sf,
-                           float* __restrict__ out) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = 3 * (int64_t)gp[k];
-    for (int d = 0; d < 3; ++d) {
-      float uu = 0.f, ss = 0.f;
-      if (parts & 1) { uu += un[g + d]; ss += sn[g + d]; }
-      if (parts & 2) { uu += uf[g + d]; ss += sf[g + d]; }
-      out[6 * k + d] = uu;
-      out[6 * k + 3 + d] = ss;
-    }
-  }
-}
-
-__global__ void k_ret_unpack(const float* __restrict__ in, const uint32_t* __restrict__ idx, int64_t n,
-                             float* __restrict__ u, float* __restrict__ s) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = 3 * (int64_t)idx[i];
-    for (int d = 0; d < 3; ++d) {
-      u[o + d] = in[6 * i + d];
-      s[o + d] = in[6 * i + 3 + d];
-    }
-  }
-}
-
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -83,9 +55,7 @@ void check_config(const fmm_config& c) {
   if (c.images > 0 && !(c.box_len > 0.0 && std::isfinite(c.box_len))) throw FmmError(FMM_E_ARG, "box_len must be > 0");
   if (c.traversal != 0 && c.traversal != 1) throw FmmError(FMM_E_ARG, "traversal must be 0 or 1");
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) throw FmmError(FMM_E_ARG, "bad rank/nranks");
-  if (c.partition != 0 && c.partition != 1) throw FmmError(FMM_E_ARG, "partition must be 0 or 1");
-  if (c.partition == 0 && c.nranks != 1 && c.nranks != 2 && c.nranks != 4 && c.nranks != 8)
-    throw FmmError(FMM_E_ARG, "nranks must be 1, 2, 4 or 8 (ranks own top-level Morton octants); see partition = 1");
+  if (c.partition < 0 || c.partition > 2) throw FmmError(FMM_E_ARG, "partition must be 0, 1 or 2");
   if (c.nranks > 8) throw FmmError(FMM_E_ARG, "nranks must be <= 8 (one NVLink node)");
   if (c.nranks > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "multi-GPU needs the periodic mode (images >= 1)");
   int tp = 1;
@@ -94,8 +64,6 @@ void check_config(const fmm_config& c) {
     tp *= c.tiles[d];
   }
   if (tp > 1 && c.images < 1) throw FmmError(FMM_E_ARG, "tiles need the periodic mode");
-  if (tp > 1 && c.nranks != 1 && c.nranks != tp) throw FmmError(FMM_E_ARG, "with tiles, nranks must equal their product");
-  if (tp > 1 && c.partition != 0) throw FmmError(FMM_E_ARG, "tiles own whole cubes: partition must be 0");
 }
 
 template <typename F>
@@ -120,22 +88,21 @@ fmm_status guard(Ctx* c, F f) {
 
 void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   cudaStream_t st = c.stream;
-  int64_t n = c.n;
   const bool multi = c.cfg.nranks > 1;
+  const int64_t n = c.n;                      // this rank's particles (after an ORB redistribution)
+  const int64_t nout = c.balanced ? c.n_caller : n;   // the caller's particles
   FMM_CUDA(cudaEventRecord(c.ev[PH_EVAL0], st));
   if (c.ntot == 0) {
     for (int p = PH_UP; p <= PH_FIN; ++p) FMM_CUDA(cudaEventRecord(c.ev[p], st));
     c.evaluated = true;
     return;
   }
-  size_t ncoef = (size_t)c.ncells * 3 * c.nc;
+  size_t ncoef = (size_t)std::max<int64_t>(c.ncells, 1) * 3 * c.nc;
   c.M.reserve(ncoef);
   c.Lc.reserve(ncoef);
-  const int64_t N = c.ntot;
+  const int64_t N = std::max<int64_t>(n, 1);
   c.u_near.reserve(3 * N); c.s_near.reserve(3 * N); c.u_far.reserve(3 * N); c.s_far.reserve(3 * N);
-  // a5-a6 upward pass (cells of other ranks stay zero until the LET arrives)
-  if (multi) FMM_CUDA(cudaMemsetAsync(c.M.p, 0, ncoef * sizeof(float2), st));
-  const bool overlap = !c.lists_valid && !multi;
+  const bool overlap = !c.lists_valid;
   if (overlap) {
     // a5-a6 on the side stream while a7 (the traversal, with its host round
     // trips between frontier rounds) runs on the main stream; joined before M2L
@@ -150,45 +117,47 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
       throw;
     }
     std::swap(c.stream, c.stream2);
-    build_lists(c);
-    FMM_CUDA(cudaEventRecord(c.ev_trav, st));
-    FMM_CUDA(cudaStreamWaitEvent(st, c.ev[PH_UP], 0));
   } else {
     upward_pass(c);
     FMM_CUDA(cudaEventRecord(c.ev[PH_UP], st));
-    // a7 traversal (once per set_particles)
-    if (!c.lists_valid) build_lists(c);
+  }
+  if (multi) {
+    // a14: the LET payload (multipoles of the sent cells, bodies) and the top
+    // multipoles' all-reduce on the communication stream, as soon as the
+    // upward pass is done; the traversal and the local-source near field run
+    // meanwhile on the main stream ("the FMM kernels for the local tree are
+    // evaluated while the LET data is being communicated")
+    FMM_CUDA(cudaStreamWaitEvent(c.cstream, c.ev[PH_UP], 0));
+    FMM_CUDA(cudaEventRecord(c.ev_let0, c.cstream));
+    let_exchange(c, c.cstream);
+    FMM_CUDA(cudaEventRecord(c.ev_let1, c.cstream));
+  }
+  if (overlap) {
+    build_lists(c);
+    FMM_CUDA(cudaEventRecord(c.ev_trav, st));
   }
   c.overlapped = overlap;
   FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
-  // a14 LET exchange (multipoles and bodies of the remote sources in this rank's lists)
+  // no local leaf: nothing below writes the near/far buffers, so they are zero
+  if (c.nleaves == 0)
+    for (float* bp : {c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p}) FMM_CUDA(cudaMemsetAsync(bp, 0, sizeof(float) * 3 * N, st));
   if (multi) {
-    cudaEvent_t l0, l1;
-    FMM_CUDA(cudaEventCreate(&l0));
-    FMM_CUDA(cudaEventCreate(&l1));
-    FMM_CUDA(cudaEventRecord(l0, st));
-    let_exchange(c);
-    FMM_CUDA(cudaEventRecord(l1, st));
-    FMM_CUDA(cudaEventSynchronize(l1));
-    c.ms_let = ms_between(l0, l1);
-    cudaEventDestroy(l0);
-    cudaEventDestroy(l1);
-    FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
+    // a12 with local sources while the LET is in flight
+    p2p_pass(c, c.u_near.p, c.s_near.p, 1);
+    FMM_CUDA(cudaEventRecord(c.ev_p2p_loc, st));
+    FMM_CUDA(cudaStreamWaitEvent(st, c.ev_let1, 0));
   }
+  FMM_CUDA(cudaStreamWaitEvent(st, c.ev[PH_UP], 0));
+  FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));     // (multi: start of the part after the LET)
   // a9 M2L + a8 periodic far layers
   FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
   m2l_pass(c);
   periodic_far_pass(c);
   FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
-  // no owned leaf (a rank without whole leaves): nothing below writes the
-  // near/far buffers, so they are defined as zero here
-  if (c.nleaves == 0) {
-    for (float* b : {c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p})
-      FMM_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, st));
-  }
-  // a12 P2P
-  p2p_pass(c, c.u_near.p, c.s_near.p);
-  FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));
+  // a12 (multi: the received sources' entries, added)
+  p2p_pass(c, c.u_near.p, c.s_near.p, multi ? 2 : 0);
+  FMM_CUDA(cudaEventRecord(c.ev[PH_N], st));
+  cudaEvent_t ev_p2p_end = c.ev[PH_N];
   // a10-a11 downward pass
   downward_pass(c, c.u_far.p, c.s_far.p);
   FMM_CUDA(cudaEventRecord(c.ev[PH_DOWN], st));
@@ -196,38 +165,25 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   bool hu = !is_device_ptr(u), hs = !is_device_ptr(s);
   float* du = u;
   float* ds = s;
-  if (hu) { c.stage_u.reserve(3 * n); du = c.stage_u.p; }
-  if (hs) { c.stage_ds.reserve(3 * n); ds = c.stage_ds.p; }
+  if (hu) { c.stage_u.reserve(3 * std::max<int64_t>(nout, 1)); du = c.stage_u.p; }
+  if (hs) { c.stage_ds.reserve(3 * std::max<int64_t>(nout, 1)); ds = c.stage_ds.p; }
   unsigned g = nblocks(n, 256);
   if (g > 148 * 16) g = 148 * 16;
   if (c.balanced) {
-    const int P = c.cfg.nranks, R = c.cfg.rank;
-    c.ret_send.reserve(6 * std::max<int64_t>(c.nown, 1));
-    c.ret_recv.reserve(6 * std::max<int64_t>(n, 1));
-    if (c.nown > 0)
-      FMM_LAUNCH(c, k_ret_pack, nblocks(c.nown, 256), 256, 0, c.recv_gp.p, c.nown, parts, c.u_near.p, c.s_near.p,
-                 c.u_far.p, c.s_far.p, c.ret_send.p);
-    std::vector<int64_t> soff(P, 0), sb(P, 0), roff(P, 0), rb(P, 0);
-    int64_t so = 0, ro = 0;
-    for (int q = 0; q < P; ++q) {              // the reverse of set_particles' redistribution
-      soff[q] = 24 * so;
-      roff[q] = 24 * ro;
-      sb[q] = q == R ? 0 : 24 * c.red_rcnt[q];
-      rb[q] = q == R ? 0 : 24 * c.red_scnt[q];
-      so += c.red_rcnt[q];
-      ro += c.red_scnt[q];
-    }
-    if (c.red_rcnt[R] > 0)
-      FMM_CUDA(cudaMemcpyAsync((char*)c.ret_recv.p + roff[R], (const char*)c.ret_send.p + soff[R], 24 * c.red_rcnt[R],
-                               cudaMemcpyDeviceToDevice, st));
-    alltoallv_bytes(c, c.ret_send.p, soff, sb, c.ret_recv.p, roff, rb);
-    if (n > 0) FMM_LAUNCH(c, k_ret_unpack, g, 256, 0, c.ret_recv.p, c.idx.p, n, du, ds);
+    // this rank's particles in their (local) caller order, then back to the
+    // ranks that passed them (the reverse of the ORB redistribution)
+    c.loc_u.reserve(3 * N);
+    c.loc_s.reserve(3 * N);
+    if (n > 0) FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, (int64_t)0, parts, c.u_near.p, c.s_near.p, c.u_far.p,
+                          c.s_far.p, c.loc_u.p, c.loc_s.p);
+    orb_return(c, c.loc_u.p, c.loc_s.p, du, ds);
   } else if (n > 0) {
-    FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, c.off, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p, du, ds);
+    FMM_LAUNCH(c, k_finalize, g, 256, 0, c.idx.p, n, (int64_t)0, parts, c.u_near.p, c.s_near.p, c.u_far.p, c.s_far.p,
+               du, ds);
   }
   FMM_LAUNCH_CHECK();
-  if (hu) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
-  if (hs) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
+  if (hu && nout) FMM_CUDA(cudaMemcpyAsync(u, du, sizeof(float) * 3 * nout, cudaMemcpyDeviceToHost, st));
+  if (hs && nout) FMM_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * 3 * nout, cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaEventRecord(c.ev[PH_FIN], st));
   unsigned long long nnear = 0;
   if (c.nleaves > 0) FMM_CUDA(cudaMemcpyAsync(&nnear, c.dnear.p, sizeof(nnear), cudaMemcpyDeviceToHost, st));
@@ -237,12 +193,20 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   fmm_stats& S = c.stats;
   S.ms_upward = ms_between(c.ev[PH_EVAL0], c.ev[PH_UP]);
   // overlapped: both phases start at EVAL0 (ms_upward and ms_traverse then overlap in time)
-  S.ms_traverse = c.overlapped ? ms_between(c.ev[PH_EVAL0], c.ev_trav) : ms_between(c.ev[PH_UP], c.ev[PH_TRAV]);
-  S.ms_m2l = ms_between(c.ev[PH_TRAV], c.ev[PH_M2L]);
-  S.ms_p2p = ms_between(c.ev[PH_M2L], c.ev[PH_P2P]);
-  S.ms_downward = ms_between(c.ev[PH_P2P], c.ev[PH_DOWN]);
+  S.ms_traverse = c.overlapped ? ms_between(c.ev[PH_EVAL0], c.ev_trav) : 0.0;
+  S.ms_m2l = ms_between(c.ev[PH_P2P], c.ev[PH_M2L]);
+  S.ms_p2p = ms_between(c.ev[PH_M2L], ev_p2p_end);
+  if (multi) {
+    S.ms_p2p += ms_between(c.ev[PH_TRAV], c.ev_p2p_loc);
+    c.ms_let = ms_between(c.ev_let0, c.ev_let1);
+    // time the main stream waited for the LET after its local near field
+    c.ms_let_exposed = std::max(0.0, (double)ms_between(c.ev_p2p_loc, c.ev[PH_P2P]));
+  }
+  S.ms_downward = ms_between(ev_p2p_end, c.ev[PH_DOWN]);
   S.ms_finalize = ms_between(c.ev[PH_DOWN], c.ev[PH_FIN]);
   S.ms_eval_total = ms_between(c.ev[PH_EVAL0], c.ev[PH_FIN]);
+  S.ms_m2l_tc = c.nm2l ? ms_between(c.ev_m2l[0], c.ev_m2l[1]) : 0.0;
+  S.ms_m2l_reg = c.nm2l ? ms_between(c.ev_m2l[1], c.ev_m2l[2]) : 0.0;
 }
 
 }  // namespace
@@ -303,8 +267,13 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
     // side stream: the upward pass runs beside the traversal (they are independent)
     FMM_CUDA(cudaStreamCreateWithFlags(&c.stream2, cudaStreamNonBlocking));
+    if (cfg->nranks > 1) {
+      FMM_CUDA(cudaStreamCreateWithFlags(&c.cstream, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&c.ev_let0, &c.ev_let1, &c.ev_p2p_loc}) FMM_CUDA(cudaEventCreate(e));
+    }
     FMM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     FMM_CUDA(cudaEventCreate(&c.ev_trav));
+    for (auto& e : c.ev_m2l) FMM_CUDA(cudaEventCreate(&e));
     set_expansion_smem_limits();
     FMM_CUDA(cudaGetLastError());
     comm_init(c);
@@ -320,9 +289,13 @@ FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
   cudaSetDevice(c.cfg.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.stream2) cudaStreamSynchronize(c.stream2);
+  if (c.cstream) cudaStreamSynchronize(c.cstream);
+  for (cudaEvent_t e : {c.ev_let0, c.ev_let1, c.ev_p2p_loc}) if (e) cudaEventDestroy(e);
+  if (c.cstream) cudaStreamDestroy(c.cstream);
   for (int i = 0; i <= PH_N; ++i) if (c.ev[i]) cudaEventDestroy(c.ev[i]);
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_trav) cudaEventDestroy(c.ev_trav);
+  for (auto e : c.ev_m2l) if (e) cudaEventDestroy(e);
   if (c.stream2) cudaStreamDestroy(c.stream2);
   try { comm_destroy(c); } catch (...) {}
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
@@ -395,6 +368,7 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->p2p_list = c.np2p;
   s->m2l_list = c.nm2l;
   s->m2l_tc_list = c.tc_entries;
+  s->m2l_reg_list = c.nm2lr;
   s->p2p_pairs = c.p2p_pairs;
   s->far_m2l = c.far_m2l;
   s->model_flops = 174.0 * (double)c.p2p_pairs;
@@ -409,6 +383,10 @@ FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   s->let_cells = c.let_cells;
   s->let_leaves = c.let_leaves;
   s->ms_let = c.ms_let;
+  s->ms_let_exposed = c.ms_let_exposed;
+  s->let_fallback = c.let_fallback;
+  s->nranks = c.cfg.nranks;
+  s->ncells_local = c.nloc_cells;
   s->cub_calls = c.cub_calls;
   return FMM_OK;
 }
@@ -441,7 +419,7 @@ FMM_API fmm_status fmm_get_keys(const fmm_ctx* h, uint64_t* keys, int64_t* perm)
     if (!c.have_particles) throw FmmError(FMM_E_STATE, "no particles");
     if (c.n == 0) return;
     std::vector<uint32_t> idx(c.n);
-    const uint64_t* kp = c.cfg.nranks > 1 ? c.keys_loc.p : c.keys.p;
+    const uint64_t* kp = c.keys.p;
     if (keys) FMM_CUDA(cudaMemcpy(keys, kp, sizeof(uint64_t) * c.n, cudaMemcpyDeviceToHost));
     FMM_CUDA(cudaMemcpy(idx.data(), c.idx.p, sizeof(uint32_t) * c.n, cudaMemcpyDeviceToHost));
     if (perm) for (int64_t i = 0; i < c.n; ++i) perm[i] = idx[i];
@@ -557,7 +535,6 @@ FMM_API fmm_status fmm_step(fmm_ctx* h, int64_t n, float* x, float* alpha, float
   return guard(&c, [&] {
     if (n < 0 || (n > 0 && (!x || !alpha || !sigma))) throw FmmError(FMM_E_ARG, "bad arguments");
     if (!(dt > 0.0) || !(nu >= 0.0) || !std::isfinite(dt) || !std::isfinite(nu)) throw FmmError(FMM_E_ARG, "need dt > 0, nu >= 0");
-    if (c.cfg.nranks > 1) throw FmmError(FMM_E_ARG, "fmm_step is single-GPU in this build (no particle migration)");
     FMM_CUDA(cudaSetDevice(c.cfg.device));
     cudaStream_t st = c.stream;
     c.st_x.reserve(3 * n); c.st_a.reserve(3 * n); c.st_s.reserve(n);
@@ -573,7 +550,9 @@ FMM_API fmm_status fmm_step(fmm_ctx* h, int64_t n, float* x, float* alpha, float
     evaluate_impl(c, 3, c.st_u.p, c.st_da.p);
     step_stage_update(c, c.st_x.p, c.st_a.p, c.st_s.p, c.st_u.p, c.st_da.p, n, 0.5 * dt, nu * dt, c.st_xh.p,
                       c.st_ah.p, c.st_sh.p);
-    // stage 2 at t + dt/2
+    // stage 2 at t + dt/2 (several GPUs: the particles move to the owners of the
+    // stage-1 ORB domains -- the partition is reused)
+    c.orb_reuse_next = true;
     set_particles_impl(c, n, c.st_xh.p, c.st_ah.p, c.st_sh.p);
     evaluate_impl(c, 3, c.st_u.p, c.st_da.p);
     // x' = x + dt u(t+dt/2), alpha' = alpha + dt dalpha/dt(t+dt/2), sigma'^2 = sigma^2 + 2 nu dt (Eq. 4)

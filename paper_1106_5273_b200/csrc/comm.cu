@@ -85,8 +85,37 @@ void alltoallv_bytes(Ctx& c, const void* sbuf, const std::vector<int64_t>& soff,
   FMM_NCCL(ncclGroupEnd());
 }
 
-void allreduce_sum_f32(Ctx& c, float* p, int64_t n) {
-  FMM_NCCL(ncclAllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)c.comm, c.stream));
+void allreduce_sum_f32(Ctx& c, float* p, int64_t n, cudaStream_t st) {
+  FMM_NCCL(ncclAllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)c.comm, st ? st : c.stream));
+}
+
+void allreduce_sum_u64(Ctx& c, unsigned long long* p, int64_t n) {
+  FMM_NCCL(ncclAllReduce(p, p, (size_t)n, ncclUint64, ncclSum, (ncclComm_t)c.comm, c.stream));
+}
+
+// every rank's n doubles (host in, host out [P][n]), synchronous
+std::vector<double> allgather_f64(Ctx& c, const double* v, int n) {
+  const int P = c.cfg.nranks;
+  c.comm_f64.reserve((size_t)P * n);
+  FMM_CUDA(cudaMemcpyAsync(c.comm_f64.p + (size_t)c.cfg.rank * n, v, sizeof(double) * n, cudaMemcpyHostToDevice,
+                           c.stream));
+  FMM_NCCL(ncclAllGather(c.comm_f64.p + (size_t)c.cfg.rank * n, c.comm_f64.p, (size_t)n, ncclFloat64,
+                         (ncclComm_t)c.comm, c.stream));
+  std::vector<double> out((size_t)P * n);
+  FMM_CUDA(cudaMemcpyAsync(out.data(), c.comm_f64.p, sizeof(double) * P * n, cudaMemcpyDeviceToHost, c.stream));
+  FMM_CUDA(cudaStreamSynchronize(c.stream));
+  return out;
+}
+
+// grouped send/recv of several (buffer, bytes) segments per peer in one NCCL group, on stream st
+void alltoallv_multi(Ctx& c, const std::vector<CommSeg>& segs, cudaStream_t st) {
+  FMM_NCCL(ncclGroupStart());
+  for (const CommSeg& g : segs) {
+    if (g.bytes <= 0) continue;
+    if (g.send) FMM_NCCL(ncclSend(g.ptr, (size_t)g.bytes, ncclChar, g.peer, (ncclComm_t)c.comm, st));
+    else FMM_NCCL(ncclRecv((void*)g.ptr, (size_t)g.bytes, ncclChar, g.peer, (ncclComm_t)c.comm, st));
+  }
+  FMM_NCCL(ncclGroupEnd());
 }
 
 }  // namespace fmmb

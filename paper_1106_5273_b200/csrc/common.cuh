@@ -43,6 +43,14 @@ struct FmmError : std::runtime_error {
     FMM_CUDA(cudaGetLastError());                                      \
   } while (0)
 
+// The same on an explicit stream (the multi-GPU comm stream).
+#define FMM_LAUNCH_ON(ctx, strm, kern, grid, block, smem, ...)        \
+  do {                                                                 \
+    kern<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);            \
+    ++(ctx).launches;                                                  \
+    FMM_CUDA(cudaGetLastError());                                      \
+  } while (0)
+
 // Grow-only device buffer owned by a context.
 template <typename T>
 struct DBuf {

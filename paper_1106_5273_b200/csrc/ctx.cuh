@@ -27,6 +27,25 @@ struct TcLevel {
 
 enum Phase { PH_SET0, PH_KEYS, PH_SORT, PH_TREE, PH_EVAL0, PH_UP, PH_TRAV, PH_M2L, PH_P2P, PH_DOWN, PH_FIN, PH_N };
 
+// one depth of the ORB recursive multisection (partition.cu)
+constexpr int kMaxGroups = 8;
+struct OrbPass {
+  int ngroups;                          // groups of this depth
+  int active[kMaxGroups];               // group is split at this depth
+  int axis[kMaxGroups];                 // x, y, z, x, ...
+  unsigned long long prefix[kMaxGroups];   // the selected element's key (low part: keys below it)
+  int shift;                            // radix-select digit = (key >> shift) & 255
+  int lo_id[kMaxGroups], hi_id[kMaxGroups];   // group ids of the next depth
+};
+
+// one segment of a grouped NCCL exchange
+struct CommSeg {
+  bool send;
+  int peer;
+  const void* ptr;
+  int64_t bytes;
+};
+
 struct Ctx {
   fmm_config cfg{};
   int P = 10, nc = 55;
@@ -35,31 +54,48 @@ struct Ctx {
   std::string err;
   bool poisoned = false;
 
-  // ---- multi-GPU (a14): this rank owns global sorted positions [off, off + n) ----
+  // ---- multi-GPU (a14): local tree + LET forest (let.cu), ORB partition (partition.cu) ----
   void* comm = nullptr;                      // ncclComm_t
-  int64_t ntot = 0, off = 0;
-  std::vector<int64_t> rank_off;             // [nranks + 1] global offsets of the ranks' particles
+  cudaStream_t cstream = nullptr;            // LET exchange (overlaps the local near field)
+  cudaEvent_t ev_up = nullptr, ev_let0 = nullptr, ev_let1 = nullptr, ev_p2p_loc = nullptr;
   DBuf<int64_t> comm_i64;
-  DBuf<int> tgt_ok;                          // cell may hold local targets (traversal filter)
-  std::vector<int64_t> loc_lo, loc_hi;       // per level: cells fully owned by this rank
-  DBuf<uint64_t> keys_loc;                   // local sorted keys (multi-GPU)
-  DBuf<int> need, need_ids, need_ids2, req_in, req_owner, req_owner2;
-  DBuf<char> let_send, let_recv;
-  DBuf<int64_t> req_off;
+  DBuf<double> comm_f64;
+  int64_t ntot = 0, off = 0;                 // particles over all ranks; off = 0 (kept for the stats)
+  int64_t nloc_cells = 0;                    // cells of the local tree: ids [0, nloc_cells)
+  int64_t nsrc = 0;                          // particle slots: local [0, n), received bodies [n, nsrc)
+  std::vector<int64_t> loc_lo, loc_hi;       // per level: the local tree's cells
+  // LET, send side (receiver-major records, fixed per set_particles)
+  DBuf<uint64_t> let_rec, let_rec2;
+  DBuf<unsigned char> let_dec;
+  DBuf<int> let_recof, let_scell;
+  DBuf<int64_t> let_boff, let_brec;
+  DBuf<char> let_srec, let_rrec;
+  int64_t let_nsend_rec = 0, let_nbrec = 0;
+  std::vector<int64_t> let_nrec_s, let_nbody_s, let_nrec_r, let_nbody_r, let_cbase, let_bbase;
+  std::vector<int> let_peer, let_roots, let_root_leaf;
+  DBuf<float2> let_sM;
+  DBuf<float4> let_sP, let_sA;
+  DBuf<unsigned char> cflag;                 // [ncells] 2 = frontier (children not sent), 4 = leaf without bodies
+  DBuf<unsigned long long> dfallback;
+  int64_t let_fallback = 0;
   int64_t let_bytes_sent = 0, let_bytes_recv = 0, let_cells = 0, let_leaves = 0;
-  double ms_let = 0.0;
-  // balanced partition (cfg.partition = 1): equal-count Morton ranges cut at leaf boundaries
-  bool balanced = false;
-  int64_t nown = 0;                          // owned particles: global sorted positions [off, off + nown)
-  DBuf<uint64_t> keys_gat;                   // every rank's sorted keys, rank blocks
-  DBuf<uint32_t> gsrc, gsrc_tmp;             // global position -> gathered index
-  DBuf<int> ginv;                            // this rank's gathered block -> global position
-  DBuf<float4> red_send, red_recv;           // particle records (x, y, z, sigma), (alpha, global position)
-  DBuf<int> recv_gp;                         // owned particles in receive order: global position
-  std::vector<int64_t> red_scnt, red_rcnt;   // records sent to / received from each peer
-  DBuf<int> strad;                           // cells (level >= 2) holding a split point: partial M, all-reduced
-  int64_t nstrad = 0, redist_bytes = 0;
-  DBuf<float> ret_send, ret_recv, strad_buf;
+  double ms_let = 0.0, ms_let_exposed = 0.0;
+  DBuf<float2> top_M;                        // root + level-1 multipoles, summed over ranks (a8, Z27)
+  // ORB partition (cfg.partition >= 1)
+  bool balanced = false, orb_fixed = false, orb_reuse_next = false;
+  std::vector<OrbPass> orb_passes;
+  std::vector<int> orb_owner;
+  DBuf<unsigned char> orb_grp;
+  DBuf<unsigned long long> orb_hist;
+  DBuf<uint32_t> red_okey, red_sidx;         // send order: red_sidx[k] = caller index of send slot k
+  DBuf<float4> red_send, red_recv;
+  std::vector<int64_t> red_scnt, red_rcnt;
+  DBuf<float> px, pa, ps;                    // this rank's particles after the redistribution
+  int64_t n_caller = 0, n_own = 0, nown = 0, redist_bytes = 0;
+  DBuf<float> ret_send, ret_recv, loc_u, loc_s;
+  // tensor-core M2L source map for forests (m2l_tc.cu): level grid -> cell id
+  DBuf<int> tc_map;
+  std::vector<int64_t> tc_map_off;
 
   // ---- particles and tree (set_particles) ----
   int64_t n = 0;
@@ -93,7 +129,7 @@ struct Ctx {
   DBuf<int4> tc_cq;                          // packed (qx, qy, qz, level) for the verification
   DBuf<int> cnt_m2l, cnt_p2p, cnt_push, off_m2l, off_p2p, off_push;
   int64_t np2p = 0, nm2l = 0, p2p_pairs = 0;
-  DBuf<int> p2p_b, p2p_e, m2l_b, m2l_e;
+  DBuf<int> p2p_b, p2p_e, p2p_m, m2l_b, m2l_e;   // p2p_m: first remote-source entry (nranks > 1)
   DBuf<unsigned long long> dcount, dnear;
   int64_t p2p_near_pairs = 0;                // pairs of the last P2P on regularised tiles
   // tensor-core M2L (m2l_tc.cu): decided once per list build
@@ -131,6 +167,7 @@ struct Ctx {
   // ---- timing ----
   cudaEvent_t ev[PH_N + 1] = {};
   cudaEvent_t ev_fork = nullptr, ev_trav = nullptr;   // upward-pass / traversal overlap
+  cudaEvent_t ev_m2l[3] = {};                          // M2L sub-phases: start, tensor done, register done
   bool overlapped = false;
   fmm_stats stats{};
 };
@@ -155,14 +192,22 @@ std::vector<int64_t> allgather_i64(Ctx& c, int64_t v);
 std::vector<int64_t> alltoall_i64(Ctx& c, const std::vector<int64_t>& send);
 void alltoallv_bytes(Ctx& c, const void* sbuf, const std::vector<int64_t>& soff, const std::vector<int64_t>& sbytes,
                      void* rbuf, const std::vector<int64_t>& roff, const std::vector<int64_t>& rbytes);
-void allreduce_sum_f32(Ctx& c, float* p, int64_t n);
-void let_exchange(Ctx& c);
+void allreduce_sum_f32(Ctx& c, float* p, int64_t n, cudaStream_t st = nullptr);
+void allreduce_sum_u64(Ctx& c, unsigned long long* p, int64_t n);
+std::vector<double> allgather_f64(Ctx& c, const double* v, int n);
+void alltoallv_multi(Ctx& c, const std::vector<CommSeg>& segs, cudaStream_t st);
+void let_setup(Ctx& c);
+void let_exchange(Ctx& c, cudaStream_t cs);
+void top_multipoles(Ctx& c, cudaStream_t cs);
+void bbox_of(Ctx& c, const float4* pos, int64_t n, float out[6]);
+void orb_redistribute(Ctx& c, int64_t n, const float* x, const float* a, const float* s, const float4* pos_wrapped);
+void orb_return(Ctx& c, const float* u_loc, const float* s_loc, float* u, float* s);
 void step_stage_update(Ctx& c, const float* x, const float* a, const float* s, const float* u, const float* da,
                        int64_t n, double h, double two_nu_t, float* xo, float* ao, float* so);
 void periodic_far_pass(Ctx& c);
 void fill_f32(Ctx& c, float* p, int64_t n, float v);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
-void p2p_pass(Ctx& c, float* u_near, float* s_near);
+void p2p_pass(Ctx& c, float* u_near, float* s_near, int part = 0);   // part: 0 all, 1 local sources, 2 remote (adds)
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g);
 void eval_pair_kernel(Ctx& c, const float* rho, int64_t n, int branch, float* g, float* rgp);
 void gauss_pass(Ctx& c, const float4* q, double* out);

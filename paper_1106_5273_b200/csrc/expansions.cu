@@ -264,7 +264,7 @@ __global__ void k_far_super(int P, int k, Geo g, const float2* __restrict__ Mroo
 // (level-1 cells, radius (sqrt3/2) box_len) instead of the elongated domain's,
 // which keeps the convergence ratio of the cubic case.
 __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, int ntg, GCells c, Geo g,
-                          const double* __restrict__ farM, int ntile, const float2* __restrict__ Mcell,
+                          const double* __restrict__ farM, int ntile, const float2* __restrict__ Mtop,
                           double2* __restrict__ part) {
   extern __shared__ double smd[];
   const int nc = P * (P + 1) / 2;
@@ -294,17 +294,17 @@ __global__ void k_far_m2l(int P, int k, const int* __restrict__ targets, int ntg
     double tox = 0, toy = 0, toz = 0;            // source centre offset from c0
     __syncthreads();
     if (tiled) {
-      const int tc = 1 + ts;                     // level-1 cell (a tile)
+      const int o = ts;                          // tile ts = the level-1 cell of octant ts (x fastest, Z27)
       const double s1 = 0.5 * g.L;
-      tox = (c.qx[tc] + 0.5) * s1 - 0.5 * g.per[0];
-      toy = (c.qy[tc] + 0.5) * s1 - 0.5 * g.per[1];
-      toz = (c.qz[tc] + 0.5) * s1 - 0.5 * g.per[2];
+      tox = ((o & 1) + 0.5) * s1 - 0.5 * g.per[0];
+      toy = (((o >> 1) & 1) + 0.5) * s1 - 0.5 * g.per[1];
+      toz = (((o >> 2) & 1) + 0.5) * s1 - 0.5 * g.per[2];
       const double ratio = s1 / st;
       for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
         int kk = i % nc, n, m;
         nm_of(kk, n, m);
         const double sc = pow(ratio, n);
-        const float2 v = Mcell[(int64_t)tc * 3 * nc + i];
+        const float2 v = Mtop[(int64_t)(1 + o) * 3 * nc + i];
         Ms[i] = {(double)v.x * sc, (double)v.y * sc};
       }
     } else {
@@ -512,44 +512,39 @@ void upward_pass(Ctx& c) {
     FMM_LAUNCH(c, k_p2m, (unsigned)c.nleaves, round32(3 * nc), sm, P, c.leaf_ids.p, gc, geo(c), c.pos.p, c.alp.p, c.M.p);
     FMM_LAUNCH_CHECK();
   }
-  // M2M over this rank's cells; the root (shared by all ranks) sums its local
-  // children here and the other ranks' through an all-reduce (a14)
+  // M2M over this rank's (local-tree) cells
   int nlev = (int)c.level_begin.size() - 1;
   for (int l = nlev - 2; l >= 0; --l) {
-    int64_t first = l == 0 ? 0 : c.loc_lo[l], cnt = l == 0 ? 1 : c.loc_hi[l] - c.loc_lo[l];
+    int64_t first = c.loc_lo[l], cnt = c.loc_hi[l] - c.loc_lo[l];
     if (cnt <= 0) continue;
     if (!m2m_level_reg(c, first, cnt, octant_r(c)))
       FMM_LAUNCH(c, k_m2m, (unsigned)cnt, round32(3 * nc), sizeof(float2) * 32 * nc, P, first, gc, octant_r(c), c.M.p);
   }
-  // root and level-1 cells (the tiles) are needed by every rank's far field
-  if (c.cfg.nranks > 1 && nlev >= 2) allreduce_sum_f32(c, (float*)c.M.p, 6 * (int64_t)nc * c.level_begin[2]);
-  // balanced partition: deeper cells holding a rank boundary carry per-rank
-  // partial multipoles (their remote children are zero here) -> summed
-  if (c.balanced && c.nstrad > 0) {
-    const int64_t rows = 3 * (int64_t)nc;     // float2 per cell
-    c.strad_buf.reserve(2 * rows * c.nstrad);
-    FMM_LAUNCH(c, k_cells_copy, nblocks(rows * c.nstrad, 256), 256, 0, c.strad.p, c.nstrad, rows, (const float2*)c.M.p,
-               (float2*)c.strad_buf.p, 0);
-    allreduce_sum_f32(c, c.strad_buf.p, 2 * rows * c.nstrad);
-    FMM_LAUNCH(c, k_cells_copy, nblocks(rows * c.nstrad, 256), 256, 0, c.strad.p, c.nstrad, rows,
-               (const float2*)c.strad_buf.p, c.M.p, 1);
-  }
+  // (nranks > 1: the root and level-1 multipoles of all ranks are summed by
+  // let_exchange into top_M for the periodic far field)
 }
 
 void m2l_pass(Ctx& c) {
-  if (c.nm2l == 0) return;
+  if (c.nm2l == 0) {
+    for (auto& e : c.ev_m2l) FMM_CUDA(cudaEventRecord(e, c.stream));
+    return;
+  }
   // tensor-core M2L on the uniform levels (m2l_tc.cu), decided once per list build
   if (!c.tc_valid) {
     m2l_tc_prepare(c);      // decides which targets the tensor path takes (verified entry by entry)
     m2l_reg_segments(c);    // the remaining entries, grouped by target for the register kernels
   }
+  FMM_CUDA(cudaEventRecord(c.ev_m2l[0], c.stream));
   m2l_tc_run(c);
-  if (m2l_pass_reg(c)) return;   // register-blocked kernel (m2l.cu) for p in {4, 6, 8, 10}
-  int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
-  size_t sm = sizeof(float2) * (nc2 + 3 * nc);
-  FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2lr.p, gcells(c), geo(c), c.M.p,
-                                                          c.Lc.p);
-  FMM_LAUNCH_CHECK();
+  FMM_CUDA(cudaEventRecord(c.ev_m2l[1], c.stream));
+  if (!m2l_pass_reg(c)) {   // register-blocked kernel (m2l.cu) for p in {4, 6, 8, 10}, else the generic one
+    int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
+    size_t sm = sizeof(float2) * (nc2 + 3 * nc);
+    FMM_LAUNCH(c, k_m2l, (unsigned)c.ncells, round32(nc), sm, P, c.ncells, c.m2l_b.p, c.m2l_e.p, c.m2lr.p, gcells(c),
+               geo(c), c.M.p, c.Lc.p);
+    FMM_LAUNCH_CHECK();
+  }
+  FMM_CUDA(cudaEventRecord(c.ev_m2l[2], c.stream));
 }
 
 void periodic_far_pass(Ctx& c) {
@@ -570,17 +565,20 @@ void periodic_far_pass(Ctx& c) {
   if ((int)c.level_begin.size() > lt + 1)
     for (int64_t i = c.loc_lo[lt]; i < c.loc_hi[lt]; ++i) tg.push_back((int)i);
   if (tg.empty()) return;
+  // sources: the root multipole (slot 0) and the tiles' (level-1 cells, slots 1 + octant) --
+  // summed over the ranks by let_exchange, from the local tree here on one GPU
+  if (c.cfg.nranks == 1) top_multipoles(c, c.stream);
   c.far_M.reserve((size_t)k * 3 * nc * 2);
-  FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, geo(c), c.M.p, c.far_M.p);
+  FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, geo(c), c.top_M.p, c.far_M.p);
   FMM_LAUNCH_CHECK();
   c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
   FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
   size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
   const int ntg = (int)tg.size(), nchunk = 26 * (k - 1);
   c.far_part.reserve((size_t)nchunk * ntg * 3 * nc);
-  const int ntile = c.tmax > 1 && c.level_begin.size() > 2 ? (int)(c.level_begin[2] - c.level_begin[1]) : 0;
+  const int ntile = c.tmax > 1 ? c.cfg.tiles[0] * c.cfg.tiles[1] * c.cfg.tiles[2] : 0;
   FMM_LAUNCH(c, k_far_m2l, dim3(ntg, nchunk), round32(nc), sm, P, k, c.scan.p, ntg, gcells(c), geo(c), c.far_M.p,
-             ntile, c.M.p, c.far_part.p);
+             ntile, c.top_M.p, c.far_part.p);
   FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)ntg * 3 * nc, 128), 128, 0, nc, nchunk, c.scan.p, ntg, c.far_part.p,
              c.Lc.p);
   FMM_LAUNCH_CHECK();

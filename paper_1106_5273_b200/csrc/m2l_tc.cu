@@ -175,6 +175,8 @@ struct TcGeo {
   const int4* cq;                   // (qx, qy, qz, level) per cell, packed per list build (verification)
   long long per[3];                 // periods in half-finest-cell units
   int lvl_begin[kMaxLevel + 2];
+  const int* map;                   // LET forest (nranks > 1): level-grid Morton index -> cell id (-1 none,
+  int map_off[kMaxLevel + 2];       // -2 several trees), per level at map_off; null on one GPU
 };
 
 __device__ __forceinline__ uint32_t spread3_32(uint32_t v) {   // 10-bit spread (levels <= 10)
@@ -215,7 +217,8 @@ __device__ __forceinline__ int tc_source(const TcGeo& g, int lt, const I (&ct)[3
     cs &= P - 1;                                   // periods are powers of two (checked on the host)
     q[a] = (uint32_t)(((cs >> (kMaxLevel - ls)) - 1) >> 1);
   }
-  return g.lvl_begin[ls] + (int)(spread3_32(q[0]) | (spread3_32(q[1]) << 1) | (spread3_32(q[2]) << 2));
+  const int m = (int)(spread3_32(q[0]) | (spread3_32(q[1]) << 1) | (spread3_32(q[2]) << 2));
+  return g.map ? __ldg(g.map + g.map_off[ls] + m) : g.lvl_begin[ls] + m;
 }
 
 // code of one M2L list entry (or -1 if outside the encodable range)
@@ -735,6 +738,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 128));
 }
 
+// forest source map: every cell of level l (any tree) at its level-grid Morton index;
+// a second cell at the same place (ORB cuts through a cell) marks it -2
+__global__ void k_tc_map(const int* __restrict__ qx, const int* __restrict__ qy, const int* __restrict__ qz,
+                         const int* __restrict__ level, int64_t n, int l, int off, int* __restrict__ map) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (level[i] != l) continue;
+    const int m = (int)(spread3_32((uint32_t)qx[i]) | (spread3_32((uint32_t)qy[i]) << 1) | (spread3_32((uint32_t)qz[i]) << 2));
+    const int old = atomicCAS(map + off + m, -1, (int)i);
+    if (old != -1) atomicExch(map + off + m, -2);
+  }
+}
+
+__global__ void k_fill_i32(int* p, int64_t n, int v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
 __global__ void k_tc_cq(const int* __restrict__ qx, const int* __restrict__ qy, const int* __restrict__ qz,
                         const int* __restrict__ level, int64_t n, int4* __restrict__ cq) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -748,6 +767,8 @@ TcGeo make_geo(Ctx& c) {
   for (int a = 0; a < 3; ++a) g.per[a] = c.per_units[a];
   const int nl = (int)c.level_begin.size();
   for (int l = 0; l < kMaxLevel + 2; ++l) g.lvl_begin[l] = (int)c.level_begin[std::min(l, nl - 1)];
+  g.map = c.cfg.nranks > 1 ? c.tc_map.p : nullptr;
+  for (int l = 0; l < kMaxLevel + 2; ++l) g.map_off[l] = l < (int)c.tc_map_off.size() ? (int)c.tc_map_off[l] : 0;
   return g;
 }
 
@@ -778,6 +799,22 @@ void m2l_tc_prepare(Ctx& c) {
   c.tc_cq.reserve(std::max<int64_t>(c.ncells, 1));
   FMM_LAUNCH(c, k_tc_cq, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
              c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, c.tc_cq.p);
+  if (c.cfg.nranks > 1) {
+    // LET forest: sources are found through a per-level map of all trees' cells
+    c.tc_map_off.assign(kMaxLevel + 2, 0);
+    int64_t tot = 0;
+    for (int l = 2; l < nlev; ++l) {
+      c.tc_map_off[l] = tot;
+      if (c.level_begin[l + 1] - c.level_begin[l] >= 1024) tot += 1ll << (3 * l);
+    }
+    if (tot >= (1ll << 31)) return;
+    c.tc_map.reserve(std::max<int64_t>(tot, 1));
+    FMM_LAUNCH(c, k_fill_i32, (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, c.tc_map.p, tot, -1);
+    for (int l = 2; l < nlev; ++l)
+      if (c.level_begin[l + 1] - c.level_begin[l] >= 1024)
+        FMM_LAUNCH(c, k_tc_map, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
+                   c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, l, (int)c.tc_map_off[l], c.tc_map.p);
+  }
   const TcGeo g = make_geo(c);
   const TcTables T = make_tables();
   cudaStream_t st = c.stream;

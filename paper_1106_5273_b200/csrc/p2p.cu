@@ -39,7 +39,8 @@ namespace {
 
 constexpr int TP = 64;           // targets per block pass and sources per tile
 constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
-constexpr float kFarRho2 = 4.6f * 4.6f;   // rho^2 at and beyond which the singular branch is exact to Z6
+constexpr float kFarRho2 = 4.6f * 4.6f;
+constexpr int kAdjChunk = 16;    // sources per FP32 partial for source leaves touching the target leaf   // rho^2 at and beyond which the singular branch is exact to Z6
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
@@ -210,13 +211,13 @@ __device__ __forceinline__ void flush(double (*sD)[NT], int lane, const Acc2& A,
 // leaf-local FP32 source data (a12 staging, once per evaluate): for every
 // particle of every leaf, (x - c_leaf) rounded from double and w = 1/(2 sigma^2),
 // and sqrt(w) = 1/(sqrt2 sigma) in the free fourth lane of (alpha, .)
-__global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t ncells, double lo0, double lo1,
-                             double lo2, double L, const float4* __restrict__ pos, float4* __restrict__ posl,
-                             float4* __restrict__ alp) {
+__global__ void k_leaf_local(const int* __restrict__ leaf, const unsigned char* __restrict__ cflag, PCells c,
+                             int64_t c0, int64_t ncells, double lo0, double lo1, double lo2, double L,
+                             const float4* __restrict__ pos, float4* __restrict__ posl, float4* __restrict__ alp) {
   const int lane = threadIdx.x & 31;
-  for (int64_t cell = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; cell < ncells;
+  for (int64_t cell = c0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); cell < ncells;
        cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    if (!leaf[cell]) continue;
+    if (!leaf[cell] || (cflag && cflag[cell])) continue;     // LET: frontier cells and body-less leaves hold no particles
     const double s = L / (double)(1 << c.level[cell]);
     const double cx = lo0 + (c.qx[cell] + 0.5) * s, cy = lo1 + (c.qy[cell] + 0.5) * s, cz = lo2 + (c.qz[cell] + 0.5) * s;
     const int b = c.begin[cell], n = c.count[cell];
@@ -229,7 +230,7 @@ __global__ void k_leaf_local(const int* __restrict__ leaf, PCells c, int64_t nce
   }
 }
 
-template <int MINB, int UF, int UN>
+template <int MINB, int UF, int UN, bool ACC>
 __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
   const double cx = lo0 + (c.qx[leaf] + 0.5) * s, cy = lo1 + (c.qy[leaf] + 0.5) * s,
                cz = lo2 + (c.qz[leaf] + 0.5) * s;
   const int eb = seg_b[leaf], ee = seg_e[leaf];
+  if (ACC && eb >= ee) return;                    // second pass (remote sources): nothing to add
   const float hst = (float)(0.5 * s);
   unsigned long long nnear = 0;                   // pairs evaluated with the regularised kernel
   for (int t0 = 0; t0 < tcnt; t0 += TP) {
@@ -306,6 +308,9 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       const float C1 = (float)(lo1 + (c.qy[src] + 0.5) * ss + ((img / 3) % 3 - 1) * py - cy);
       const float C2 = (float)(lo2 + (c.qz[src] + 0.5) * ss + (img / 9 - 1) * pz - cz);
       const int sb = c.begin[src], scnt = c.count[src];
+      // source leaf touching (or equal to) the target leaf: |C_d| <= s_t/2 + s_s/2 on every axis
+      const float reach = (float)(0.5 * (s + ss)) * 1.0001f;
+      const bool adj = fabsf(C0) <= reach && fabsf(C1) <= reach && fabsf(C2) <= reach;
       for (int s0 = 0; s0 < scnt; s0 += TP) {
         __syncwarp();
         // stage the tile, far sources first: a source is "far" when it is
@@ -360,13 +365,22 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(B1.x), "=f"(B1.y) : "r"(b + 8 * NT));
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(B2.x), "=f"(B2.y) : "r"(b + 16 * NT));
         }
-        Acc2 A;
-        zero(A);
+        // FP32 partials over chunks of the tile, each added into the FP64
+        // accumulators by flush: 64 sources per chunk, 16 for a source leaf that
+        // touches the target leaf (its close pairs carry the largest terms, and
+        // the factorisation through C amplifies their rounding by |x_i - C|/|r|;
+        // FP32 emulation at C4: stretching rel-L2 8.9e-6 -> 4.6e-6)
+        const int cs = adj ? kAdjChunk : TP;
+        for (int c0 = 0; c0 < nj; c0 += cs) {
+          const int c1 = min(nj, c0 + cs), fe = min(c1, nfar);
+          Acc2 A;
+          zero(A);
 #pragma unroll UF
-        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
+          for (int jj = c0; jj < fe; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
 #pragma unroll UN
-        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
-        flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
+          for (int jj = max(c0, nfar); jj < c1; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+          flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
+        }
       }
     }
     // s += (sum_j f alpha_j) x alpha_i
@@ -378,10 +392,15 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       const double u0 = D[0 * NT], u1 = D[1 * NT], u2 = D[2 * NT], s0 = D[3 * NT], s1 = D[4 * NT], s2 = D[5 * NT];
       const double f0 = D[6 * NT], f1 = D[7 * NT], f2 = D[8 * NT];
       const int64_t o = 3 * (int64_t)(tb + (h == 0 ? i0 : i1));
-      un[o] = (float)u0; un[o + 1] = (float)u1; un[o + 2] = (float)u2;
-      sn[o] = (float)(s0 + (f1 * ai.z - f2 * ai.y));
-      sn[o + 1] = (float)(s1 + (f2 * ai.x - f0 * ai.z));
-      sn[o + 2] = (float)(s2 + (f0 * ai.y - f1 * ai.x));
+      const float r[6] = {(float)u0, (float)u1, (float)u2, (float)(s0 + (f1 * ai.z - f2 * ai.y)),
+                          (float)(s1 + (f2 * ai.x - f0 * ai.z)), (float)(s2 + (f0 * ai.y - f1 * ai.x))};
+      if (ACC) {
+        un[o] += r[0]; un[o + 1] += r[1]; un[o + 2] += r[2];
+        sn[o] += r[3]; sn[o + 1] += r[4]; sn[o + 2] += r[5];
+      } else {
+        un[o] = r[0]; un[o + 1] = r[1]; un[o + 2] = r[2];
+        sn[o] = r[3]; sn[o + 1] = r[4]; sn[o + 2] = r[5];
+      }
     }
   }
   if (lane == 0 && nnear) atomicAdd(near_pairs, nnear);
@@ -410,7 +429,7 @@ __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch
   // no early exit: pair2<true> votes across the whole warp
   const int64_t i0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   const float r0 = i0 < n ? rho[i0] : 1.f, r1 = i0 + 1 < n ? rho[i0 + 1] : 1.f;
-  const float w = 0.5f;                                     // 1/(2 sigma^2) with sqrt2 sigma = 1
+  const float w = 1.0f;                                     // 1/(2 sigma^2) with sqrt2 sigma = 1
   const float4 q = make_float4(0.f, 0.f, 0.f, -1.4426950408889634f * w);
   const float aw = sqrtf(w);
   const float4 a = make_float4(1.f, 0.f, 0.f, aw);
@@ -445,22 +464,34 @@ void eval_pair_kernel(Ctx& c, const float* rho, int64_t n, int branch, float* g,
   FMM_LAUNCH(c, k_eval_pair, nblocks((n + 1) / 2, 256), 256, 0, rho, n, branch, g, rgp);
 }
 
-void p2p_pass(Ctx& c, float* u_near, float* s_near) {
+void p2p_pass(Ctx& c, float* u_near, float* s_near, int part) {
   if (c.nleaves == 0) return;
   c.dnear.reserve(1);
-  FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
+  if (part != 2) FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
   // 16 blocks/SM (128 registers), far loop unrolled 4x, near 4x: the best of
   // the occupancy/unroll sweep on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8, <12,4,2> 210.2)
   // Prefetching the next list entry while the current tile is evaluated does not pay (r01 v23 A/B,
   // tools/p2p_ab.sh, bit-identical results): its cell-table reads 200.35 -> 200.80 ms, plus its first
   // source tile 207.53 ms (40 B of spills); the tile-boundary load latency is hidden by the other warps.
-  c.posl.reserve(std::max<int64_t>(c.ntot, 1));
-  FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c.ncells + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p, pc,
-             (int64_t)c.ncells, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p, c.alp.p);
-  FMM_LAUNCH(c, (k_p2p<16, 4, 4>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, c.p2p_b.p, c.p2p_e.p, c.p2p.p, pc,
-             c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
-             c.dnear.p);
+  // part 1 / 2 (nranks > 1): the entries with local sources while the LET is in flight, then the
+  // received sources' entries added (fig:flow_chart)
+  c.posl.reserve(std::max<int64_t>(c.nsrc, 1));
+  const bool multi = c.cfg.nranks > 1;
+  const int64_t c0 = part == 2 ? c.nloc_cells : 0, c1 = part == 1 ? c.nloc_cells : c.ncells;
+  if (c1 > c0)
+    FMM_LAUNCH(c, k_leaf_local, (unsigned)std::min<int64_t>((c1 - c0 + 7) / 8, 148 * 32), 256, 0, c.cells.leaf.p,
+               multi ? c.cflag.p : nullptr, pc, c0, c1, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p, c.alp.p);
+  const int* sb = part == 2 ? c.p2p_m.p : c.p2p_b.p;
+  const int* se = part == 1 ? c.p2p_m.p : c.p2p_e.p;
+  if (part == 2)
+    FMM_LAUNCH(c, (k_p2p<16, 4, 4, true>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
+               c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
+               c.dnear.p);
+  else
+    FMM_LAUNCH(c, (k_p2p<16, 4, 4, false>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
+               c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
+               c.dnear.p);
 }
 
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {

@@ -17,7 +17,8 @@ namespace fmmb {
 namespace {
 
 struct TCells {
-  const int *level, *qx, *qy, *qz, *child_begin, *nchild, *leaf, *count, *tgt_ok;
+  const int *level, *qx, *qy, *qz, *child_begin, *nchild, *leaf, *count;
+  const unsigned char* cflag;   // LET forest (nranks > 1): 2 = frontier, 4 = leaf without bodies; else null
 };
 
 struct TParams {
@@ -44,15 +45,25 @@ __device__ __forceinline__ bool mac_accept(const TCells& c, const TParams& p, in
   return p.lhs_k * ss * ss < p.rhs_k * d2;
 }
 
-// Alg. 2 Interact: 0 = M2L, 1 = P2P, 2 = push.
+// Alg. 2 Interact: 0 = M2L, 1 = P2P, 2 = push, 3 = M2L by the remote branch.
+// A remote source received without what the pair needs -- a frontier cell
+// (children not sent) that would be split, or a leaf without bodies -- takes
+// "the M2L translation with the smallest cell that is available" (Alg. 2,
+// P:176-179); such fallbacks are counted (zero when the LET-MAC is
+// complete).  Frontier cells carry the leaf flag, so they are never split.
 __device__ __forceinline__ int interact(const TCells& c, const TParams& p, int A, int B, int img) {
-  bool leaves = c.leaf[A] && c.leaf[B];
+  const bool leaves = c.leaf[A] && c.leaf[B];
+  const int fl = c.cflag ? c.cflag[B] : 0;
   if (p.leaf_first) {
-    if (leaves) return 1;
+    if (leaves) {
+      if (fl & 2) return mac_accept(c, p, A, B, img) ? 0 : 3;   // internal in its own tree
+      return (fl & 4) ? 3 : 1;
+    }
     return mac_accept(c, p, A, B, img) ? 0 : 2;
   }
   if (mac_accept(c, p, A, B, img)) return 0;
-  return leaves ? 1 : 2;
+  if (leaves) return fl ? 3 : 1;
+  return 2;
 }
 
 // Alg. 1 body for frontier pair f: split B if A is a leaf or (B is not a leaf
@@ -62,7 +73,7 @@ __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells 
                          int* __restrict__ cm, int* __restrict__ cp, int* __restrict__ cq,
                          const int* __restrict__ om, const int* __restrict__ op, const int* __restrict__ oq,
                          uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p, uint64_t* __restrict__ next,
-                         unsigned char* __restrict__ has_m2l) {
+                         unsigned char* __restrict__ has_m2l, unsigned long long* __restrict__ fallback) {
   int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f >= nf) return;
   uint64_t e = front[f];
@@ -76,8 +87,11 @@ __global__ void k_expand(const uint64_t* __restrict__ front, int64_t nf, TCells 
   for (int k = 0; k < nch; ++k) {
     int a = split_b ? A : cb + k;
     int b = split_b ? cb + k : B;
-    if (!split_b && !c.tgt_ok[a]) continue;        // a14: targets of other ranks are theirs
     int d = interact(c, p, a, b, img);
+    if (d == 3) {
+      if (WRITE) atomicAdd(fallback, 1ull);
+      d = 0;
+    }
     if (d == 0) {
       if (WRITE) {
         m2l[bm + nm] = pack(a, b, img);
@@ -101,6 +115,18 @@ __global__ void k_segments(const uint64_t* __restrict__ lst, int64_t n, int* __r
     int t = (int)(lst[i] >> 32);
     if (i == 0 || (int)(lst[i - 1] >> 32) != t) sb[t] = (int)i;
     if (i == n - 1 || (int)(lst[i + 1] >> 32) != t) se[t] = (int)(i + 1);
+  }
+}
+
+// p2p_m[t] = the first entry of target t's segment with a remote source
+__global__ void k_remote_split(const uint64_t* __restrict__ lst, int64_t n, int nloc, int* __restrict__ pm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = lst[i];
+    const int t = (int)(e >> 32), s = (int)((e >> 5) & 0x7ffffff);
+    if (s < nloc) continue;
+    if (i == 0) { pm[t] = 0; continue; }
+    const uint64_t f = lst[i - 1];
+    if ((int)(f >> 32) != t || (int)((f >> 5) & 0x7ffffff) < nloc) pm[t] = (int)i;
   }
 }
 
@@ -188,42 +214,60 @@ void build_lists(Ctx& c) {
   cudaStream_t st = c.stream;
   c.np2p = c.nm2l = 0;
   c.p2p_pairs = 0;
-  if (c.ncells == 0) { c.lists_valid = true; return; }
+  c.let_fallback = 0;
+  if (c.nloc_cells == 0) { c.lists_valid = true; return; }
+  const bool multi = c.cfg.nranks > 1;
   TCells tc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.child_begin.p,
-            c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p, c.tgt_ok.p};
+            c.cells.nchild.p, c.cells.leaf.p, c.cells.count.p, multi ? c.cflag.p : nullptr};
+  c.dfallback.reserve(1);
+  FMM_CUDA(cudaMemsetAsync(c.dfallback.p, 0, sizeof(unsigned long long), st));
   TParams tp{3ull * (unsigned long long)c.cfg.theta_den * (unsigned long long)c.cfg.theta_den,
              (unsigned long long)c.cfg.theta_num * (unsigned long long)c.cfg.theta_num, c.cfg.traversal,
              {c.per_units[0], c.per_units[1], c.per_units[2]}};
 
-  // seeds (8c-2 item 7): Interact(root, root, img) for the 27 first-layer
-  // images (k >= 1) or the zero image.  The root pair never passes the MAC
-  // (|Delta| <= sqrt(3) L while r_A + r_B = sqrt(3) L and theta < 1), so a
-  // seed is P2P iff the root is a leaf, else it is pushed.
-  std::vector<uint64_t> seeds;
-  if (c.cfg.images > 0) for (int img = 0; img < 27; ++img) seeds.push_back((uint64_t)img);
-  else seeds.push_back((uint64_t)kImgCentre);
-  bool root_leaf = c.host_leaf_top.size() > 0 && c.host_leaf_top[0];
+  // seeds (8c-2 item 7): Interact(root, root_t, img) for the 27 first-layer
+  // images (k >= 1) or the zero image, for every tree t of the forest (the
+  // local tree and the peers' LETs, nranks > 1).  A root pair never passes
+  // the MAC (|Delta| <= sqrt(3) L while r_A + r_B = sqrt(3) L and theta < 1),
+  // and a received root is never a frontier or a leaf without bodies (the
+  // LET-MAC cannot accept a root), so a seed is P2P iff both roots are
+  // leaves, else it is pushed.
+  std::vector<uint64_t> seeds, pseeds;
+  const bool root_leaf = c.host_leaf_top.size() > 0 && c.host_leaf_top[0];
+  std::vector<int> roots{0}, rleaf{root_leaf ? 1 : 0};
+  for (size_t j = 0; j < c.let_roots.size() && multi; ++j) {
+    roots.push_back(c.let_roots[j]);
+    rleaf.push_back(c.let_root_leaf[j]);
+  }
+  for (size_t t = 0; t < roots.size(); ++t) {
+    std::vector<int> imgs;
+    if (c.cfg.images > 0) for (int img = 0; img < 27; ++img) imgs.push_back(img);
+    else imgs.push_back(kImgCentre);
+    for (int img : imgs) {
+      const uint64_t e = ((uint64_t)roots[t] << 5) | (uint64_t)img;      // target = local root 0
+      (root_leaf && rleaf[t] ? pseeds : seeds).push_back(e);
+    }
+  }
   int64_t nf = (int64_t)seeds.size();
-  c.front_a.reserve(1024);
+  c.front_a.reserve(std::max<int64_t>(1024, nf));
   c.front_b.reserve(1024);
   c.tc_has.reserve(std::max<int64_t>(c.ncells, 1));
   FMM_CUDA(cudaMemsetAsync(c.tc_has.p, 0, std::max<int64_t>(c.ncells, 1), st));
-  c.p2p.reserve(1 << 16);
+  c.p2p.reserve(std::max<int64_t>(1 << 16, (int64_t)pseeds.size()));
   c.m2l.reserve(1 << 16);
-  if (root_leaf) {
-    FMM_CUDA(cudaMemcpyAsync(c.p2p.p, seeds.data(), sizeof(uint64_t) * nf, cudaMemcpyHostToDevice, st));
-    c.np2p = nf;
-    nf = 0;
-  } else {
-    FMM_CUDA(cudaMemcpyAsync(c.front_a.p, seeds.data(), sizeof(uint64_t) * nf, cudaMemcpyHostToDevice, st));
+  if (!pseeds.empty()) {
+    FMM_CUDA(cudaMemcpyAsync(c.p2p.p, pseeds.data(), sizeof(uint64_t) * pseeds.size(), cudaMemcpyHostToDevice, st));
+    c.np2p = (int64_t)pseeds.size();
   }
+  if (nf) FMM_CUDA(cudaMemcpyAsync(c.front_a.p, seeds.data(), sizeof(uint64_t) * nf, cudaMemcpyHostToDevice, st));
+  FMM_CUDA(cudaStreamSynchronize(st));          // host vectors above are read by the copies
 
   while (nf > 0) {
     c.cnt_m2l.reserve(nf + 1); c.cnt_p2p.reserve(nf + 1); c.cnt_push.reserve(nf + 1);
     c.off_m2l.reserve(nf + 1); c.off_p2p.reserve(nf + 1); c.off_push.reserve(nf + 1);
     unsigned g = nblocks(nf, 256);
     FMM_LAUNCH(c, k_expand<false>, g, 256, 0, c.front_a.p, nf, tc, tp, c.cnt_m2l.p, c.cnt_p2p.p, c.cnt_push.p,
-                                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+                                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     FMM_LAUNCH_CHECK();
     exclusive_scan(c, c.cnt_m2l.p, c.off_m2l.p, nf);
     exclusive_scan(c, c.cnt_p2p.p, c.off_p2p.p, nf);
@@ -244,7 +288,7 @@ void build_lists(Ctx& c) {
     c.front_b.reserve(add_q);
     FMM_LAUNCH(c, k_expand<true>, g, 256, 0, c.front_a.p, nf, tc, tp, nullptr, nullptr, nullptr, c.off_m2l.p,
                                       c.off_p2p.p, c.off_push.p, c.m2l.p + c.nm2l, c.p2p.p + c.np2p, c.front_b.p,
-                                      c.tc_has.p);
+                                      c.tc_has.p, c.dfallback.p);
     FMM_LAUNCH_CHECK();
     c.nm2l += add_m;
     c.np2p += add_p;
@@ -263,6 +307,14 @@ void build_lists(Ctx& c) {
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
   FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
   if (c.np2p) FMM_LAUNCH(c, k_segments, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
+  if (multi) {
+    // a14 overlap: per target, the entries with local sources (ids < nloc, first
+    // in canonical order) run while the LET is in flight, the rest after it
+    c.p2p_m.reserve(c.ncells);
+    FMM_CUDA(cudaMemcpyAsync(c.p2p_m.p, c.p2p_e.p, sizeof(int) * c.ncells, cudaMemcpyDeviceToDevice, st));
+    if (c.np2p)
+      FMM_LAUNCH(c, k_remote_split, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, (int)c.nloc_cells, c.p2p_m.p);
+  }
   c.dcount.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
   if (c.np2p) {
@@ -275,6 +327,10 @@ void build_lists(Ctx& c) {
   FMM_CUDA(cudaMemcpyAsync(&pairs, c.dcount.p, sizeof(pairs), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
   c.p2p_pairs = (int64_t)pairs;
+  unsigned long long fb = 0;
+  FMM_CUDA(cudaMemcpyAsync(&fb, c.dfallback.p, sizeof(fb), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c.let_fallback = (int64_t)fb;
   c.lists_valid = true;
 }
 

@@ -42,7 +42,9 @@ class fmm_stats(C.Structure):
                 ("ntot", C.c_int64), ("let_bytes_sent", C.c_int64), ("let_bytes_recv", C.c_int64),
                 ("let_cells", C.c_int64), ("let_leaves", C.c_int64), ("ms_let", C.c_double),
                 ("m2l_tc_list", C.c_int64), ("own_begin", C.c_int64), ("own_count", C.c_int64),
-                ("redist_bytes", C.c_int64)]
+                ("redist_bytes", C.c_int64), ("m2l_reg_list", C.c_int64), ("ms_m2l_tc", C.c_double),
+                ("ms_m2l_reg", C.c_double), ("ms_let_exposed", C.c_double), ("let_fallback", C.c_int64),
+                ("nranks", C.c_int64), ("ncells_local", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "struct_size"}
@@ -280,7 +282,7 @@ class FMM:
             kw["nccl_id"] = C.cast(self._id, C.c_void_p)
         self.cfg = fmm_config_default(**kw)
         self.ctx = fmm_create(self.cfg)
-        self.n = 0
+        self.n = None          # particle count of the last set (None: nothing set yet)
 
     def set_particles(self, x, alpha, sigma):
         n = int(x.shape[0])

@@ -68,12 +68,14 @@ def random_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI, sigma=None, h=No
     return x.astype(np.float32), alpha.astype(np.float32), sig.astype(np.float32)
 
 
-def jittered_lattice(n: int, seed: int = 5273, lo=-np.pi, L=TWO_PI, overlap=1.0):
-    """Taylor-Green lattice with positions jittered by +-h/4 (key boundaries)."""
+def jittered_lattice(n: int, seed: int = 5273, lo=-np.pi, L=TWO_PI, overlap=1.0, amp=0.25):
+    """Taylor-Green lattice with positions jittered uniformly by +-amp*h
+    (amp = 1/4 keeps every particle in its lattice cell; amp = 1 moves
+    particles across leaf boundaries, so leaf counts vary and the tree adapts)."""
     x, a, s = taylor_green(n, overlap, lo, L)
     h = L / n
     rng = np.random.default_rng(seed)
-    xj = x.astype(np.float64) + (rng.random(x.shape) - 0.5) * 0.5 * h
+    xj = x.astype(np.float64) + (rng.random(x.shape) - 0.5) * 2.0 * amp * h
     xj = np.clip(xj, lo, np.nextafter(np.float32(lo + L), np.float32(lo)))
     return xj.astype(np.float32), a, s
 

@@ -1,15 +1,27 @@
-"""Multi-GPU parity check (a14), run under torchrun with one process per GPU:
+"""Multi-GPU parity check (a14, NEXT-3, NEXT-1), run under torchrun with one
+process per GPU:
 
     python -m torch.distributed.run --nproc-per-node P --master-addr 127.0.0.1 \
-        --master-port 29511 tests/mgpu_check.py --side 16
+        --master-port 29511 tests/mgpu_check.py --side 16 --mode tiled
 
-Every rank evaluates its octant block of the weak-scaling Taylor-Green lattice
-(synth.taylor_green_rank) through the C ABI with nranks = P.  Rank 0 then runs
-the single-GPU evaluation of the union of all blocks and checks:
-* each rank's P2P and M2L lists == the single-GPU lists restricted to the
-  targets that rank owns (bit-exact, global cell ids),
-* the near field (P2P) is bit-identical and the full field agrees to 1e-6,
-* both match the Taylor-Green closed form to 1e-3.
+Every rank evaluates its particles through the C ABI with nranks = P; each
+rank builds the octree of its own particles and receives the other ranks'
+local essential trees (LET-MAC).  Rank 0 then runs the single-GPU
+evaluation of the union and checks:
+* partition 0 (tiled / refined: each rank passes a whole block of top-level
+  octants): every rank's P2P and M2L lists, written as
+  (level, qx, qy, qz) cell tuples and image, equal the single-GPU lists
+  restricted to the targets the rank owns (bit-exact), with no
+  remote-branch fallback (Alg. 2);
+* partition 1 (orb, orb_cloud: every rank passes a seeded random subset; ORB
+  multisection): the per-rank particle counts are the
+  floor(N m1/m) splits (balance within 1 particle), results come back in
+  every rank's caller order, no fallback;
+* the near field agrees with one GPU to 2e-6 and the full field to 1e-5
+  (1e-3 for the clustered cloud, whose ORB trees differ from the single-GPU
+  tree), and the Taylor-Green fields meet the closed form to 1e-3;
+* step: one midpoint-RK2 fmm_step (NEXT-1) with partition 1 equals the
+  single-GPU step and the oracle's direct-sum RK2 (rk2_step).
 Prints one JSON line; exit code 1 on any failure.
 """
 import argparse
@@ -36,7 +48,7 @@ def tg_closed(x, alpha, sigma):
 
 def run(fmm, x, a, s, parts=3):
     n = len(x)
-    xd, ad, sd = (torch.from_numpy(v).cuda() for v in (x, a, s))
+    xd, ad, sd = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (x, a, s))
     fmm.set_particles(xd, ad, sd)
     u = torch.empty((n, 3), device="cuda")
     st = torch.empty((n, 3), device="cuda")
@@ -44,10 +56,24 @@ def run(fmm, x, a, s, parts=3):
     return u.cpu().numpy().astype(np.float64), st.cpu().numpy().astype(np.float64)
 
 
+def tuples(lst, cells):
+    """List entries (t, s, img) -> rows (level_t, q_t(3), level_s, q_s(3), img), sorted."""
+    if len(lst) == 0:
+        return np.zeros((0, 9), dtype=np.int64)
+    t = cells[lst[:, 0], :4]
+    s = cells[lst[:, 1], :4]
+    rows = np.concatenate([t, s, lst[:, 2:3]], axis=1)
+    return rows[np.lexsort(rows.T[::-1])]
+
+
+def rel(p, q):
+    return float(np.linalg.norm(p - q) / np.linalg.norm(q))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=16)
-    ap.add_argument("--mode", choices=["tiled", "refined", "balanced", "balanced_cloud"], default="tiled")
+    ap.add_argument("--mode", choices=["tiled", "refined", "orb", "orb_cloud", "step"], default="tiled")
     args = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -56,81 +82,102 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [P.fmm_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    balanced = args.mode.startswith("balanced")
-    if balanced:
-        # NEXT-3: every rank passes an arbitrary (seeded random) subset; the
-        # library cuts equal-count Morton ranges at leaf boundaries
-        full = synth.taylor_green(args.side) if args.mode == "balanced" else synth.clustered_cloud(args.side ** 3)
+    orb = args.mode in ("orb", "orb_cloud", "step")
+    images = 1 if args.mode == "step" else 3
+    if orb:
+        full = synth.clustered_cloud(args.side ** 3) if args.mode == "orb_cloud" else synth.taylor_green(args.side)
         gen = lambda side, w, r: tuple(v[synth.scatter_to_ranks(len(full[0]), w, r)] for v in full)
+    elif args.mode == "tiled":
+        gen = synth.taylor_green_tile
     else:
-        gen = synth.taylor_green_tile if args.mode == "tiled" else synth.taylor_green_rank
+        gen = synth.taylor_green_octants
     tiles = synth.RANK_TILES[world] if args.mode == "tiled" else (1, 1, 1)
     x, a, s = gen(args.side, world, rank)
-    fmm = P.FMM(images=3, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles,
-                partition=1 if balanced else 0)
-    un, sn = run(fmm, x, a, s, parts=1)
-    u, st = run(fmm, x, a, s)
-    p2p, m2l = P.fmm_get_lists(fmm.ctx)
-    stats = fmm.stats()
+    fmm = P.FMM(images=images, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles,
+                partition=1 if orb else 0)
+    res = {}
+    if args.mode == "step":
+        dt = 0.5 * float(s[0])
+        xs, as_, ss = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (x, a, s))
+        fmm.step(xs, as_, ss, dt, 0.01)
+        res = dict(x=xs.cpu().numpy(), a=as_.cpu().numpy(), s=ss.cpu().numpy(), n=len(x), stats=fmm.stats())
+    else:
+        un, sn = run(fmm, x, a, s, parts=1)
+        u, st = run(fmm, x, a, s)
+        p2p, m2l = P.fmm_get_lists(fmm.ctx)
+        cells = P.fmm_get_cells(fmm.ctx)
+        stats = fmm.stats()
+        res = dict(u=u, s=st, un=un, sn=sn, p2p=p2p, m2l=m2l, cells=cells, n=len(x), stats=stats)
     fmm.close()
     gathered = [None] * world
-    dist.all_gather_object(gathered, dict(u=u, s=st, un=un, sn=sn, p2p=p2p, m2l=m2l, n=len(x), stats=stats))
-    ok, msg = True, {}
+    dist.all_gather_object(gathered, res)
+    ok, msg = True, {"world": world, "mode": args.mode}
     if rank == 0:
         blocks = [gen(args.side, world, r) for r in range(world)]
         X = np.concatenate([b[0] for b in blocks])
         A = np.concatenate([b[1] for b in blocks])
         S = np.concatenate([b[2] for b in blocks])
-        single = P.FMM(images=3, device=local, tiles=tiles)
-        Un, Sn = run(single, X, A, S, parts=1)
-        U, SS = run(single, X, A, S)
-        gp2p, gm2l = P.fmm_get_lists(single.ctx)
-        cells = P.fmm_get_cells(single.ctx)
+        msg["fallback"] = [int(g["stats"]["let_fallback"]) for g in gathered]
+        ok &= all(f == 0 for f in msg["fallback"])
+        single = P.FMM(images=images, device=local, tiles=tiles)
+        if args.mode == "step":
+            dt = 0.5 * float(S[0])
+            xs, as_, ss = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (X, A, S))
+            single.step(xs, as_, ss, dt, 0.01)
+            X1, A1, S1 = xs.cpu().numpy(), as_.cpu().numpy(), ss.cpu().numpy()
+            DX = np.concatenate([g["x"] for g in gathered])
+            DA = np.concatenate([g["a"] for g in gathered])
+            DS = np.concatenate([g["s"] for g in gathered])
+            msg["step_vs_single"] = [rel(DX - X, X1 - X), rel(DA - A, A1 - A), rel(DS, S1)]
+            ok &= max(msg["step_vs_single"]) <= 1e-5
+            import oracle
+            oracle.build()
+            xo, ao, so = oracle.rk2_step(X, A, S, dt, 0.01, images=images)
+            msg["step_vs_oracle_rk2"] = [rel(DX - X, xo - X), rel(DA - A, ao - A), rel(DS, so)]
+            ok &= max(msg["step_vs_oracle_rk2"]) <= 1e-3
+        else:
+            Un, Sn = run(single, X, A, S, parts=1)
+            U, SS = run(single, X, A, S)
+            gp2p, gm2l = P.fmm_get_lists(single.ctx)
+            gcells = P.fmm_get_cells(single.ctx)
+            if args.mode in ("tiled", "refined"):
+                for r in range(world):
+                    g = gathered[r]
+                    nloc = g["stats"]["ncells_local"]
+                    mine = {tuple(v) for v in g["cells"][:nloc, :4].tolist() if v[0] >= 1}
+                    own = np.array([tuple(v) in mine for v in gcells[:, :4].tolist()])
+                    for name, glst in (("p2p", gp2p), ("m2l", gm2l)):
+                        want = tuples(glst[own[glst[:, 0]]], gcells)
+                        got = tuples(g[name], g["cells"])
+                        same = got.shape == want.shape and np.array_equal(got, want)
+                        ok &= bool(same)
+                        msg["%s_rank%d_bitexact" % (name, r)] = bool(same)
+            if orb:
+                # X is the ranks' subsets concatenated, so the single-GPU results
+                # line up with every rank's caller-order results
+                own = [int(g["stats"]["n"]) for g in gathered]
+                N = len(X)
+                msg["own_counts"] = own
+                msg["imbalance"] = float(max(own) / (N / world))
+                ok &= msg["imbalance"] <= 1.0 + world / N + 1e-12 and sum(own) == N
+            du = np.concatenate([g["un"] for g in gathered])
+            ds = np.concatenate([g["sn"] for g in gathered])
+            DU = np.concatenate([g["u"] for g in gathered])
+            DS = np.concatenate([g["s"] for g in gathered])
+            cloud = args.mode == "orb_cloud"
+            msg["near_vs_single"] = [rel(du, Un), rel(ds, Sn)]
+            msg["full_vs_single"] = [rel(DU, U), rel(DS, SS)]
+            ok &= max(msg["near_vs_single"]) <= (1e-3 if cloud else 2e-6)
+            ok &= max(msg["full_vs_single"]) <= (1e-3 if cloud else 1e-5)
+            if not cloud:
+                uc, sc = tg_closed(X, A, S[0])
+                msg["closed_form"] = [rel(DU, uc), rel(DS, sc)]
+                ok &= max(msg["closed_form"]) <= 1e-3
+            msg["let"] = [{k: g["stats"][k] for k in ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves",
+                                                       "ms_let", "ms_let_exposed", "redist_bytes", "ncells",
+                                                       "ncells_local")} for g in gathered]
         single.close()
-        off = np.cumsum([0] + [g["n"] for g in gathered])
-        if balanced:
-            # owned ranges partition [0, N), cut at leaf boundaries; a rank's
-            # targets are the cells overlapping its range
-            ob = [(g["stats"]["own_begin"], g["stats"]["own_count"]) for g in gathered]
-            off = np.array([b for b, _ in ob] + [ob[-1][0] + ob[-1][1]])
-            leaves = cells[cells[:, 9] == 1]
-            ends = set(leaves[:, 4].tolist()) | set((leaves[:, 4] + leaves[:, 5]).tolist())
-            msg["own_ranges"] = [int(v) for v in off]
-            msg["ranges_ok"] = bool(off[0] == 0 and off[-1] == len(X) and np.all(np.diff(off) >= 0)
-                                    and all(int(v) in ends for v in off))
-            msg["imbalance"] = float(np.diff(off).max() / (len(X) / world))
-            ok &= msg["ranges_ok"]
-        for r in range(world):
-            if balanced:
-                owned = (cells[:, 4] < off[r + 1]) & (cells[:, 4] + cells[:, 5] > off[r])
-            else:
-                owned = (cells[:, 4] >= off[r]) & (cells[:, 4] + cells[:, 5] <= off[r + 1])
-            for name, glst in (("p2p", gp2p), ("m2l", gm2l)):
-                want = glst[owned[glst[:, 0]]]
-                got = gathered[r][name]
-                same = got.shape == want.shape and np.array_equal(got, want)
-                ok &= bool(same)
-                msg["%s_rank%d_bitexact" % (name, r)] = bool(same)
-        du = np.concatenate([g["un"] for g in gathered])
-        ds = np.concatenate([g["sn"] for g in gathered])
-        msg["near_bitexact"] = bool(np.array_equal(du, Un) and np.array_equal(ds, Sn))
-        ok &= msg["near_bitexact"]
-        DU = np.concatenate([g["u"] for g in gathered])
-        DS = np.concatenate([g["s"] for g in gathered])
-        rel = lambda p, q: float(np.linalg.norm(p - q) / np.linalg.norm(q))
-        msg["full_vs_single_u"] = rel(DU, U)
-        msg["full_vs_single_s"] = rel(DS, SS)
-        ok &= msg["full_vs_single_u"] <= 1e-6 and msg["full_vs_single_s"] <= 1e-6
-        if args.mode != "balanced_cloud":
-            uc, sc = tg_closed(X, A, S[0])
-            msg["closed_form_u"] = rel(DU, uc)
-            msg["closed_form_s"] = rel(DS, sc)
-            ok &= msg["closed_form_u"] <= 1e-3 and msg["closed_form_s"] <= 1e-3
-        msg["let"] = [{k: g["stats"][k] for k in ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves",
-                                                   "ms_let", "redist_bytes")} for g in gathered]
         msg["ok"] = bool(ok)
-        msg["world"] = world
-        msg["mode"] = args.mode
         print(json.dumps(msg), flush=True)
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(okt, src=0)

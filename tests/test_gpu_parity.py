@@ -96,8 +96,11 @@ def test_expansions_and_far_field(runs, oracle_mod, name):
            np.linalg.norm(Mg - Mo) / np.linalg.norm(Mo), np.linalg.norm(Lg - Lo) / np.linalg.norm(Lo)))
     assert np.linalg.norm(uf - r["u_far"]) / np.linalg.norm(r["u"]) <= 1e-5
     assert np.linalg.norm(sf - r["s_far"]) / np.linalg.norm(r["s"]) <= 1e-5
-    assert ef[0] <= 5e-5
-    assert ef[1] <= 5e-5
+    # self-relative: the far field is a small remainder of cancelling
+    # contributions in the leaf-first / theta = 0.4 cases (DESIGN.md reading
+    # F1: measured <= 1.12e-5, jitter10_k2_leaf_first stretching)
+    assert ef[0] <= 2e-5
+    assert ef[1] <= 2e-5
 
 
 @pytest.mark.parametrize("name", ["tg12_k1_ncrit16", "rand3000_free", "rand2500_k1_theta0.4"])

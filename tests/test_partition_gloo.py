@@ -1,16 +1,23 @@
-"""CPU (gloo, world_size 2) model of the multi-GPU host logic of a14, checked
-against the CPU oracle: Morton-octant ownership, target-side pruning of the
-dual traversal, and the exact LET request sets.
+"""CPU (gloo) models of the multi-GPU host logic of a14 and NEXT-3, checked
+against the CPU oracle and numpy:
 
-Each rank builds the oracle tree of the global particle set, keeps the list
-entries whose target it owns, derives the remote sources it must receive
-(multipoles for M2L sources, bodies for P2P source leaves) grouped by owner,
-and exchanges the request counts with gloo all-to-all.  Checked:
-* the ranks' lists partition the global lists (each entry exactly once);
-* every request goes to the rank that owns the requested cell, and the counts
-  each rank sends equal the counts its peer receives;
-* with its own and the requested sources, every owned target particle is
-  covered exactly N * 27^k times (the counting kernel of S:313).
+* ORB multisection (partition.cu): every rank holds a random
+  subset of a clustered cloud; the distributed nth-element is the same radix
+  select the library runs (8-bit digits of (order-preserving coordinate bits,
+  rank << 28 | index), one all-reduce of per-group histograms per digit), the
+  groups split at floor(N m1 / m) along x, y, z, ...  Checked: every selected
+  key is the exact k-th smallest of the group (numpy partition on the
+  gathered keys), final counts are the floor splits, the boxes are disjoint
+  along each cut.
+* LET completeness (let.cu): with Morton-octant ownership, every
+  rank builds the oracle tree of ITS OWN particles, walks it against the other
+  rank's bounding box with the library's LET-MAC ((3 + 2 theta) r_B <
+  theta d_B over the first-layer images) and sends the cell tuples; the
+  receiver checks, on the global tree's lists restricted to its own targets,
+  that every remote M2L source is in the received LET and every remote P2P
+  source leaf came with its bodies (so the remote branch of Alg. 2 is never
+  taken), and that received + local sources cover each owned target exactly
+  N 27^k times (the counting kernel of S:313).
 """
 import os
 
@@ -23,153 +30,206 @@ import torch.multiprocessing as mp
 import synth
 
 
-def _worker(rank, world, port, q):
+def _fbits(v):
+    u = np.asarray(v, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    neg = (u & 0x80000000) != 0
+    return np.where(neg, (~u) & 0xffffffff, u | 0x80000000)
+
+
+def _orb_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, a, s = synth.clustered_cloud(4000)
+        mine = synth.scatter_to_ranks(len(x), world, rank)
+        xm = x[mine]
+        ids = (np.uint64(rank) << np.uint64(28)) | np.arange(len(xm), dtype=np.uint64)
+        grp = np.zeros(len(xm), dtype=np.int64)
+        groups = [(0, world, len(x))]
+        ok = True
+        sel_log = []
+        for depth in range(8):
+            if not any(hi - lo > 1 for lo, hi, _ in groups):
+                break
+            axis = depth % 3
+            keys = (_fbits(xm[:, axis]) << np.uint64(32)) | ids
+            act = [hi - lo > 1 for lo, hi, _ in groups]
+            kth = [cnt * ((hi - lo) // 2) // (hi - lo) if hi - lo > 1 else 0 for lo, hi, cnt in groups]
+            prefix = [np.uint64(0)] * len(groups)
+            for ps in range(8):
+                shift = np.uint64(56 - 8 * ps)
+                hist = np.zeros((len(groups), 256), dtype=np.int64)
+                for g in range(len(groups)):
+                    if not act[g]:
+                        continue
+                    sel = grp == g
+                    k = keys[sel]
+                    if ps > 0:
+                        up = np.uint64(64 - 8 * ps)
+                        k = k[(k >> up) == (prefix[g] >> up)]
+                    np.add.at(hist[g], ((k >> shift) & np.uint64(255)).astype(np.int64), 1)
+                th = torch.from_numpy(hist)
+                dist.all_reduce(th)
+                hist = th.numpy()
+                for g in range(len(groups)):
+                    if not act[g] or groups[g][2] == 0:
+                        continue
+                    c = np.cumsum(hist[g])
+                    d = int(np.searchsorted(c, kth[g], side="right"))
+                    kth[g] -= int(c[d - 1]) if d > 0 else 0
+                    prefix[g] = prefix[g] | (np.uint64(d) << shift)
+            # check: the selected key is the exact k-th smallest of the gathered group keys
+            allk = [None] * world
+            dist.all_gather_object(allk, (keys, grp))
+            nxt = []
+            newgrp = grp.copy()
+            for g, (lo, hi, cnt) in enumerate(groups):
+                if not act[g]:
+                    newgrp[grp == g] = len(nxt)
+                    nxt.append((lo, hi, cnt))
+                    continue
+                gk = np.concatenate([k[gg == g] for k, gg in allk])
+                m1 = (hi - lo) // 2
+                nlow = cnt * m1 // (hi - lo)
+                ok &= bool(len(gk) == cnt)
+                if cnt:
+                    ok &= bool(np.sort(gk)[nlow] == prefix[g])
+                    sel_log.append(int(prefix[g] >> np.uint64(32)))
+                low = (grp == g) & (keys < prefix[g])
+                newgrp[low] = len(nxt)
+                nxt.append((lo, lo + m1, nlow))
+                newgrp[(grp == g) & ~(keys < prefix[g])] = len(nxt)
+                nxt.append((lo + m1, hi, cnt - nlow))
+            grp = newgrp
+            groups = nxt
+        own = np.array([groups[g][0] for g in range(len(groups))])[grp]
+        cnt = torch.tensor(np.bincount(own, minlength=world), dtype=torch.int64)
+        dist.all_reduce(cnt)
+        N = len(x)
+        ok &= int(cnt.sum()) == N and int(cnt.max()) - int(cnt.min()) <= 1 + N // world - N // world
+        ok &= bool(np.all(np.abs(cnt.numpy() - N / world) <= 1.0))
+        q.put((rank, bool(ok), [int(v) for v in cnt], sel_log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_orb_radix_select_three_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    port = 29670
+    procs = [ctx.Process(target=_orb_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] for r in res), res
+    assert len({tuple(r[2]) for r in res}) == 1
+
+
+def _cell_geom(cells, lo, L):
+    s = L / (2.0 ** cells[:, 0])
+    c = lo + (cells[:, 1:4] + 0.5) * s[:, None]
+    return c, s
+
+
+def _let_walk(cells, lo, L, box, theta, per):
+    """The LET-MAC walk of let.cu on an oracle tree: {(level, q): bodies?}."""
+    ctr, side = _cell_geom(cells, lo, L)
+    coef = (3.0 + 2.0 * theta) / theta
+    shifts = np.array([[(i % 3 - 1) * per, ((i // 3) % 3 - 1) * per, (i // 9 - 1) * per] for i in range(27)])
+    out = {}
+    stack = [0]
+    while stack:
+        c = stack.pop()
+        cc = ctr[c][None, :] + shifts
+        d = np.maximum(0, np.maximum(box[0] - cc, cc - box[1]))
+        dmin = np.sqrt((d * d).sum(1)).min()
+        acc = coef * 0.8660254037844386 * side[c] * (1 + 1e-9) < dmin
+        key = tuple(int(v) for v in cells[c, :4])
+        if cells[c, 9]:
+            out[key] = not acc
+        elif acc:
+            out[key] = False
+        else:
+            out[key] = False
+            stack.extend(range(cells[c, 7], cells[c, 7] + cells[c, 8]))
+    return out
+
+
+def _let_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle
-        blocks = [synth.taylor_green_rank(6, world, r) for r in range(world)]
-        x = np.concatenate([b[0] for b in blocks])
-        a = np.concatenate([b[1] for b in blocks])
-        s = np.concatenate([b[2] for b in blocks])
-        f = oracle.OracleFMM(x, a, s, images=1, ncrit=8)
-        cells = f.cells()
-        p2p, m2l = f.p2p_list(), f.m2l_list()
-        n = np.array([len(b[0]) for b in blocks])
-        off = np.concatenate([[0], np.cumsum(n)])
-        b0, cnt = cells[:, 4], cells[:, 5]
-        owned = (b0 >= off[rank]) & (b0 + cnt <= off[rank + 1])
-        mine_p2p = p2p[owned[p2p[:, 0]]]
-        mine_m2l = m2l[owned[m2l[:, 0]]]
-        owner = np.searchsorted(off, b0, side="right") - 1
-        need_m = np.unique(mine_m2l[:, 1][~owned[mine_m2l[:, 1]]])
-        need_p = np.unique(mine_p2p[:, 1][~owned[mine_p2p[:, 1]]])
+        side, theta, L = 8, 0.5, 2 * np.pi
+        lo = np.full(3, -np.pi)
+        blocks = [synth.taylor_green_octants(side, world, r) for r in range(world)]
+        x, a, s = blocks[rank]
+        mine = oracle.OracleFMM(x, a, s, images=1, ncrit=8)
+        cells_m = mine.cells()
+        box = np.array([x.min(0), x.max(0)], dtype=np.float64)
+        boxes = [None] * world
+        dist.all_gather_object(boxes, box)
+        lets = {r: _let_walk(cells_m, lo, L, boxes[r], theta, L) for r in range(world) if r != rank}
+        got = [None] * world
+        dist.all_gather_object(got, lets)
+        recv = {}
+        for r in range(world):
+            if r != rank:
+                recv.update(got[r][rank])
+        # the global tree's lists restricted to my targets
+        X = np.concatenate([b[0] for b in blocks])
+        A = np.concatenate([b[1] for b in blocks])
+        S = np.concatenate([b[2] for b in blocks])
+        g = oracle.OracleFMM(X, A, S, images=1, ncrit=8)
+        gc = g.cells()
+        p2p, m2l = g.p2p_list(), g.m2l_list()
+        key = [tuple(int(v) for v in r[:4]) for r in gc]
+        mykeys = {tuple(int(v) for v in r[:4]) for r in cells_m if r[0] >= 1}
+        owned = np.array([k in mykeys for k in key])
         ok = True
-        # requests go to the owner of the whole requested cell
-        for cid in np.concatenate([need_m, need_p]):
-            q_ = owner[cid]
-            ok &= bool(q_ != rank and b0[cid] >= off[q_] and b0[cid] + cnt[cid] <= off[q_ + 1])
-        send = torch.zeros(world, dtype=torch.int64)
-        for cid in np.concatenate([need_m, need_p]):
-            send[owner[cid]] += 1
-        recv = torch.zeros(world, dtype=torch.int64)
-        dist.all_to_all_single(recv, send)
-        allsend = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(allsend, send)
-        for p_ in range(world):
-            ok &= int(recv[p_]) == int(allsend[p_][rank])
-        # coverage of owned targets with local + received sources
-        cover = np.zeros(len(x), dtype=np.int64)
-        for (t, src, _img) in mine_p2p:
-            cover[b0[t]:b0[t] + cnt[t]] += cnt[src]
-        for (t, src, _img) in mine_m2l:
-            cover[b0[t]:b0[t] + cnt[t]] += cnt[src]
-        mine = np.arange(off[rank], off[rank + 1])
-        ok &= bool(np.all(cover[mine] == len(x) * 27))
-        # the ranks' lists partition the global lists
-        sizes = torch.tensor([len(mine_p2p), len(mine_m2l)], dtype=torch.int64)
-        dist.all_reduce(sizes)
-        ok &= int(sizes[0]) == len(p2p) and int(sizes[1]) == len(m2l)
-        q.put((rank, bool(ok), int(len(need_m)), int(len(need_p))))
+        nremote = 0
+        for t, src, _img in m2l[owned[m2l[:, 0]]]:
+            if key[src] in mykeys:
+                continue
+            nremote += 1
+            ok &= key[src] in recv
+        for t, src, _img in p2p[owned[p2p[:, 0]]]:
+            if key[src] in mykeys:
+                continue
+            nremote += 1
+            ok &= bool(recv.get(key[src], False))
+        # coverage of my targets with local + received sources
+        b0, cnt = gc[:, 4], gc[:, 5]
+        cover = np.zeros(len(X), dtype=np.int64)
+        for lst in (p2p, m2l):
+            for t, src, _img in lst[owned[lst[:, 0]]]:
+                cover[b0[t]:b0[t] + cnt[t]] += cnt[src]
+        _, perm = g.keys()
+        off = np.cumsum([0] + [len(b[0]) for b in blocks])
+        gpos = np.empty(len(X), dtype=np.int64)
+        gpos[perm] = np.arange(len(X))
+        me = gpos[off[rank]:off[rank + 1]]
+        ok &= bool(np.all(cover[me] == len(X) * 27))
+        q.put((rank, bool(ok), nremote, len(recv)))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_let_requests_gloo():
+def test_two_rank_let_mac_complete_gloo():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     world = 2
     port = 29650
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_let_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] for r in res), res
-    assert all(r[2] + r[3] > 0 for r in res), res      # a real exchange happens
-
-
-def _balanced_worker(rank, world, port, q):
-    """Model of the balanced partition (cfg.partition = 1, NEXT-3):
-    every rank holds a random subset of a clustered cloud; the Morton curve of
-    the global tree is cut into equal-count ranges moved to the nearest leaf
-    boundary (the library's k_splits rule), particles are sent to their owners
-    (counts exchanged with gloo) and straddling cells are the only partial
-    multipoles."""
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        import oracle
-        x, a, s = synth.clustered_cloud(3000)
-        mine = synth.scatter_to_ranks(len(x), world, rank)
-        f = oracle.OracleFMM(x, a, s, images=1, ncrit=16)
-        cells = f.cells()
-        _keys, perm = f.keys()                  # perm[g] = input index at global position g
-        N = len(x)
-        b0, cnt, leaf = cells[:, 4], cells[:, 5], cells[:, 9]
-        cb, nch = cells[:, 7], cells[:, 8]
-
-        def split(k):                           # the leaf holding k N / P, nearer boundary
-            xk = k * N // world
-            c = 0
-            while not leaf[c]:
-                kids = range(cb[c], cb[c] + nch[c])
-                c = next((ch for ch in kids if xk < b0[ch] + cnt[ch]), cb[c] + nch[c] - 1)
-            return b0[c] if xk - b0[c] <= b0[c] + cnt[c] - xk else b0[c] + cnt[c]
-
-        off = np.array([0] + [split(k) for k in range(1, world)] + [N])
-        ok = bool(np.all(np.diff(off) >= 0))
-        # no leaf is cut
-        lv = np.nonzero(leaf)[0]
-        for k in range(1, world):
-            ok &= not bool(np.any((b0[lv] < off[k]) & (off[k] < b0[lv] + cnt[lv])))
-        # balance: every range within one leaf of N / P
-        ok &= bool(np.all(np.abs(np.diff(off) - N / world) <= 2 * 16 + 1))
-        # redistribution counts: my particles' global positions -> owners
-        gpos = np.empty(N, dtype=np.int64)
-        gpos[perm] = np.arange(N)
-        owner = np.searchsorted(off, gpos[mine], side="right") - 1
-        send = torch.tensor(np.bincount(owner, minlength=world), dtype=torch.int64)
-        recv = torch.zeros(world, dtype=torch.int64)
-        dist.all_to_all_single(recv, send)
-        ok &= int(recv.sum()) == int(off[rank + 1] - off[rank])
-        # straddling cells: non-leaves only, nested (at most one per level per split)
-        st = np.zeros(len(cells), dtype=bool)
-        for k in range(1, world):
-            st |= (b0 < off[k]) & (off[k] < b0 + cnt)
-        ok &= not bool(np.any(st & (leaf == 1)))
-        lev = cells[:, 0]
-        for k in range(1, world):
-            sk = (b0 < off[k]) & (off[k] < b0 + cnt)
-            ok &= bool(np.all(np.bincount(lev[sk]) <= 1))
-        # M is linear: the per-rank partial multipoles of a straddling cell
-        # (its particles split by owner) sum to the full one -- modelled on the
-        # monopole (sum of alpha) of every straddling cell
-        for c in np.nonzero(st)[0]:
-            idx = perm[b0[c]:b0[c] + cnt[c]]
-            gp = np.arange(b0[c], b0[c] + cnt[c])
-            mono = torch.tensor(a[idx[(gp >= off[rank]) & (gp < off[rank + 1])]].astype(np.float64).sum(0))
-            dist.all_reduce(mono)
-            ok &= bool(np.allclose(mono.numpy(), a[idx].astype(np.float64).sum(0), rtol=1e-12, atol=1e-18))
-        q.put((rank, bool(ok), int(st.sum()), [int(v) for v in off]))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_three_rank_balanced_partition_gloo():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    world = 3
-    port = 29660
-    procs = [ctx.Process(target=_balanced_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=300) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-    assert all(r[1] for r in res), res
-    assert all(r[2] > 0 for r in res), res              # the splits cut through some cells
-    assert len({tuple(r[3]) for r in res}) == 1, res    # all ranks agree on the ranges
+    assert all(r[2] > 0 and r[3] > 0 for r in res), res      # a real exchange happens
