@@ -57,10 +57,10 @@ def parse():
                     help="N > 1: tiled = C5 weak scaling (one 2pi tile of side^3 per GPU, reading Z27); "
                          "refined = the fixed box refined to side*(1..2) per axis; "
                          "strong = C4: one side^3 lattice split over the GPUs by Morton octants")
-    ap.add_argument("--partition", choices=["octant", "balanced"], default="octant",
-                    help="N > 1 with --mode strong: octant = each rank passes its Morton-octant block; balanced = "
+    ap.add_argument("--partition", choices=["octant", "orb"], default="octant",
+                    help="N > 1 with --mode strong: octant = each rank passes its Morton-octant block; orb = "
                          "each rank passes a random 1/N subset and the library redistributes it every step "
-                         "(cfg.partition = 1: equal-count Morton ranges cut at leaf boundaries, NEXT-3)")
+                         "(cfg.partition = 1: ORB recursive multisection by a distributed nth-element, NEXT-3)")
     ap.add_argument("--workload", choices=["lattice", "jitter", "advected"], default="lattice",
                     help="N = 1 stress variants of C3 (VERDICT r01): jitter = the lattice jittered by +-h "
                          "(seed 5273); advected = the lattice after one fmm_step (midpoint RK2, dt = 2h, "
@@ -254,9 +254,9 @@ def main():
     tiles = synth.RANK_TILES[world] if tiled else (1, 1, 1)
     gen = {"tiled": synth.taylor_green_tile, "refined": synth.taylor_green_rank,
            "strong": synth.taylor_green_octants}[args.mode]
-    balanced = world > 1 and args.partition == "balanced"
+    balanced = world > 1 and args.partition == "orb"
     if balanced and args.mode != "strong":
-        raise SystemExit("--partition balanced needs --mode strong")
+        raise SystemExit("--partition orb needs --mode strong")
     if balanced:
         full = synth.taylor_green(args.side)
         x, a, s = (v[synth.scatter_to_ranks(len(full[0]), world, rank)] for v in full)
@@ -446,17 +446,19 @@ def main():
                        ("C4 strong scaling: Taylor-Green %d^3 in [-pi,pi)^3 %s, %d particles on "
                         "this GPU, periodic k=%d, p=%d, theta=%s, ncrit=%d" %
                         (args.side, "passed as random 1/N subsets and redistributed by the library every step "
-                         "(balanced partition: equal-count Morton ranges cut at leaf boundaries)" if balanced else
+                         "(ORB recursive multisection, partition = 1)" if balanced else
                          "split by Morton octants", n, args.images, args.order, args.theta, args.ncrit)),
                        "particles_total": int(tot_n), "step": "fmm_set_particles + fmm_evaluate (all 8a rows)",
                        "l2": "inputs larger than L2 (%.0f MB vs 126 MB); no flush" % (n * 28 / 1e6),
                        "parallelism": "1 GPU" if world == 1 else
-                       "%d GPUs: %s domain decomposition, exact LET (multipoles + bodies) over "
-                       "NCCL grouped send/recv, root multipole all-reduce" %
-                       (world, "balanced Morton-range (partition = 1)" if balanced else "Morton-octant")},
+                       "%d GPUs: %s domain decomposition, local trees + LET-MAC local essential trees "
+                       "(cells, multipoles, bodies) over NCCL grouped send/recv on a comm stream overlapped "
+                       "with the local near field, top multipoles all-reduced" %
+                       (world, "ORB multisection (partition = 1)" if balanced else "Morton-octant / tile")},
             "let": None if world == 1 else {k: statistics.mean(st[k] for st in stats) for k in
                                             ("let_bytes_sent", "let_bytes_recv", "let_cells", "let_leaves", "ms_let",
-                                             "redist_bytes")},
+                                             "ms_let_exposed", "let_fallback", "redist_bytes", "ncells",
+                                             "ncells_local")},
             "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
             "particles_per_s": tot_n / (ms_max * 1e-3),
             "phases_ms": phase,

@@ -807,7 +807,7 @@ void m2l_tc_prepare(Ctx& c) {
       c.tc_map_off[l] = tot;
       if (c.level_begin[l + 1] - c.level_begin[l] >= 1024) tot += 1ll << (3 * l);
     }
-    if (tot >= (1ll << 31)) return;
+    if (tot >= (1ll << 31) || tot == 0) return;
     c.tc_map.reserve(std::max<int64_t>(tot, 1));
     FMM_LAUNCH(c, k_fill_i32, (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, c.tc_map.p, tot, -1);
     for (int l = 2; l < nlev; ++l)

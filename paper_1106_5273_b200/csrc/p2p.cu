@@ -452,9 +452,22 @@ __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch
     const bool sing = branch == 0 && rr[h] * rr[h] >= kFarRho2;
     if (rr[h] <= 0.f) { g[i] = 0.f; rgp[i] = 0.f; continue; }       // r = 0 contributes nothing (Z7)
     const double gd = sing ? 1.0 : (double)fn[h] / (double)ff[h];
-    const double pd = sing ? 1.0 : (double)pn[h] / (double)pf[h];
+    double rg;
+    if (sing) {
+      rg = 0.0;
+    } else if (rr[h] * rr[h] < 0.64f) {
+      // series branch: f'/r from T(x); 3 g - rho g' = 3 fp_reg/fp_sing (no cancellation here)
+      rg = 3.0 * gd - 3.0 * (double)pn[h] / (double)pf[h];
+    } else {
+      // erfcx branch: fp/(-3) = c.z e/r^2 + f/r^2, so rho g' = (4/sqrt pi) rho^3 e with the
+      // kernel's e = ex2.approx(-rho^2 log2 e) (pair2's r^2 and q.w; read directly, since
+      // 3 g - 3 fp_reg/fp_sing cancels to FP32 resolution when g -> 1)
+      const float r2 = rr[h] * rr[h];
+      const float e = ex2_approx(r2 * q.w);
+      rg = 2.2567583341910251 * (double)e * (double)rr[h] * (double)rr[h] * (double)rr[h];
+    }
     g[i] = (float)gd;
-    rgp[i] = (float)(3.0 * gd - 3.0 * pd);
+    rgp[i] = (float)rg;
   }
 }
 

@@ -134,10 +134,11 @@ def taylor_green_octants(n: int, nranks: int, rank: int, lo=-np.pi, L=TWO_PI):
     return x[keep], a[keep], s[keep]
 
 
-def clustered_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI):
+def clustered_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI, sigma=None):
     """Non-uniform workload for the balanced partition (NEXT-3): half the
     particles uniform in the periodic cube, half in a Gaussian cluster of
-    width L/16 (wrapped), alpha ~ N(0,1) h^3 with h = L / n^(1/3), sigma = h."""
+    width L/16 (wrapped), alpha ~ N(0,1) h^3 with h = L / n^(1/3), sigma = h
+    (or the given sigma)."""
     rng = np.random.default_rng(seed)
     h = L / round(n ** (1.0 / 3.0))
     m = n // 2
@@ -145,7 +146,7 @@ def clustered_cloud(n: int, seed: int = 1106, lo=-np.pi, L=TWO_PI):
     xc = lo + np.mod(0.3 * L + rng.normal(0.0, L / 16, size=(m, 3)), L)
     x = np.concatenate([xu, xc]).astype(np.float32)
     a = (rng.standard_normal((n, 3)) * h ** 3).astype(np.float32)
-    s = np.full(n, h, dtype=np.float32)
+    s = np.full(n, h if sigma is None else sigma, dtype=np.float32)
     return x, a, s
 
 
