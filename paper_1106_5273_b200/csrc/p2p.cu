@@ -40,7 +40,10 @@ namespace {
 constexpr int TP = 64;           // targets per block pass and sources per tile
 constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
 constexpr float kFarRho2 = 4.6f * 4.6f;
-constexpr int kAdjChunk = 16;    // sources per FP32 partial for source leaves touching the target leaf   // rho^2 at and beyond which the singular branch is exact to Z6
+constexpr int kAdjChunk = 32;    // sources per FP32 partial for source leaves touching the target leaf
+#ifndef P2P_ADJ_MODE
+#define P2P_ADJ_MODE 1
+#endif   // rho^2 at and beyond which the singular branch is exact to Z6
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
@@ -311,7 +314,12 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
       // source leaf touching (or equal to) the target leaf: |C_d| <= s_t/2 + s_s/2 on every axis
       const float reach = (float)(0.5 * (s + ss)) * 1.0001f;
       const bool adj = fabsf(C0) <= reach && fabsf(C1) <= reach && fabsf(C2) <= reach;
-      for (int s0 = 0; s0 < scnt; s0 += TP) {
+#if P2P_ADJ_MODE == 1
+      const int tstep = adj ? kAdjChunk : TP;     // touching leaf: FP32 partials over 32 sources (below)
+#else
+      const int tstep = TP;
+#endif
+      for (int s0 = 0; s0 < scnt; s0 += tstep) {
         __syncwarp();
         // stage the tile, far sources first: a source is "far" when it is
         // >= 4.6 sqrt2 sigma_j from the whole target leaf cube, so every pair
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int j = s0 + lane + h * NT;
-          vj[h] = j < scnt;
+          vj[h] = j < scnt && j < s0 + tstep;
           fj[h] = false;
           if (vj[h]) {
             const float4 p = posl[sb + j];               // (y - C, 1/(2 sigma^2))
@@ -365,11 +373,13 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(B1.x), "=f"(B1.y) : "r"(b + 8 * NT));
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(B2.x), "=f"(B2.y) : "r"(b + 16 * NT));
         }
-        // FP32 partials over chunks of the tile, each added into the FP64
-        // accumulators by flush: 64 sources per chunk, 16 for a source leaf that
-        // touches the target leaf (its close pairs carry the largest terms, and
-        // the factorisation through C amplifies their rounding by |x_i - C|/|r|;
-        // FP32 emulation at C4: stretching rel-L2 8.9e-6 -> 4.6e-6)
+        // FP32 partials added into the FP64 accumulators by flush: per tile of
+        // 64 sources, or 32 for a source leaf that touches the target leaf (its
+        // close pairs carry the largest terms, and the factorisation through C
+        // amplifies their rounding by |x_i - C|/|r|; FP32 emulation at C4:
+        // stretching rel-L2 8.9e-6 -> 4.6e-6).  P2P_ADJ_MODE 1 stages
+        // such a leaf in tiles of 32 (emulation: 6.2e-6; 16: 4.6e-6 at +2 ms more); mode 0 chunks the loops; mode 2 does neither.
+#if P2P_ADJ_MODE == 0
         const int cs = adj ? kAdjChunk : TP;
         for (int c0 = 0; c0 < nj; c0 += cs) {
           const int c1 = min(nj, c0 + cs), fe = min(c1, nfar);
@@ -381,6 +391,15 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
           for (int jj = max(c0, nfar); jj < c1; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
           flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
         }
+#else
+        Acc2 A;
+        zero(A);
+#pragma unroll UF
+        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
+#pragma unroll UN
+        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+        flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
+#endif
       }
     }
     // s += (sum_j f alpha_j) x alpha_i
