@@ -7,15 +7,19 @@
 // against the receiver's domain (the bounding box of its particles):
 //
 //   accept B (send its multipole, do not open it) iff
-//       (3 + 2 theta) r_B < theta d_B,   d_B = min over the first-layer images
-//                                              of |c_B + shift - box_q|.
+//       (1 + theta) max(2 r_B, rleaf_q) + r_B < theta d_B,
+//       d_B = min over the first-layer images of |c_B + shift - box_q|.
 //
 // Reading Z25: the paper assumes the target cell has the source's
 // size (r_A = r_B) and its centre on the box edge.  The receiver's traversal
 // (Alg. 1, split the larger cell) only meets B against targets with r_A <= 2 r_B
 // unless the target is a leaf, and a target cell's centre can lie up to r_A
 // outside the box of its particles, so its MAC r_A + r_B < theta R_AB holds
-// whenever (1 + theta) 2 r_B + r_B < theta d_B -- the test above.  Leaves are
+// whenever (1 + theta) 2 r_B + r_B < theta d_B -- the test above.  Larger leaf
+// targets (adaptive trees: the receiver's leaves near this rank's domain are
+// coarser than this rank's cells) are covered by replacing 2 r_B with
+// max(2 r_B, rleaf_q), the radius of the largest leaf of q that can meet a
+// cell of this rank (k_leaf_reach; one int per pair of ranks).  Leaves are
 // sent with their bodies unless accepted (MAC-first) or always (leaf-first,
 // where leaf pairs are P2P before any MAC).  The receiver's traversal counts
 // every pair it cannot resolve with what it received (Alg. 2's remote branch,
@@ -54,9 +58,10 @@ struct LetCells {
 
 struct LetGeo {
   double lo[3], L, per[3];
-  double coef;            // (3 + 2 theta) / theta
+  double theta;
   int leaf_first;
   double blo[8][3], bhi[8][3];
+  double rleaf[8];        // receiver q: largest radius of its leaves that can meet cells of this rank (k_leaf_reach)
 };
 
 // record sent to the receiver: geometry, count, flags and links within the list
@@ -93,7 +98,8 @@ __global__ void k_let_count(const uint64_t* __restrict__ front, int64_t nf, LetC
     dmin2 = fmin(dmin2, box_dist2(cc, g, q));
   }
   const double r = 0.8660254037844386 * s;
-  const double lhs = g.coef * r * (1.0 + 1e-9);
+  const double ra = fmax(2.0 * r, g.rleaf[q]);              // the largest target B can meet there
+  const double lhs = ((1.0 + g.theta) * ra + r) / g.theta * (1.0 + 1e-9);
   const bool acc = lhs * lhs < dmin2;
   int d, k = 0;
   if (c.leaf[cell]) d = (g.leaf_first || !acc) ? D_BODIES : D_MONLY;
@@ -101,6 +107,33 @@ __global__ void k_let_count(const uint64_t* __restrict__ front, int64_t nf, LetC
   else { d = D_OPEN; k = c.nchild[cell]; }
   dec[f] = (unsigned char)d;
   nch[f] = k;
+}
+
+// the largest radius of this rank's leaves that can be paired with a smaller
+// cell B (r_B < r_A / 2) of rank q's domain: only a leaf target keeps meeting
+// ever smaller sources (Alg. 1 never splits a leaf), and it fails the MAC with
+// B only if R < (r_A + r_B)/theta, with R >= d(c_A, box_q) - r_B; so leaves
+// with d(c_A, box_q) < (1.5/theta + 0.5) r_A count (first-layer images included)
+__global__ void k_leaf_reach(const int* __restrict__ leaf_ids, int64_t nl, LetCells c, LetGeo g, int P, int R,
+                             unsigned* __restrict__ rmax) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nl; k += (int64_t)gridDim.x * blockDim.x) {
+    const int cell = leaf_ids[k];
+    const int l = c.level[cell];
+    const double s = g.L / (double)(1 << l);
+    const double ctr[3] = {g.lo[0] + (c.qx[cell] + 0.5) * s, g.lo[1] + (c.qy[cell] + 0.5) * s,
+                           g.lo[2] + (c.qz[cell] + 0.5) * s};
+    const double r = 0.8660254037844386 * s, reach = (1.5 / g.theta + 0.5) * r * (1.0 + 1e-9);
+    for (int q = 0; q < P; ++q) {
+      if (q == R) continue;
+      double dmin2 = 1e300;
+      for (int img = 0; img < 27; ++img) {
+        const double cc[3] = {ctr[0] + (img % 3 - 1) * g.per[0], ctr[1] + ((img / 3) % 3 - 1) * g.per[1],
+                              ctr[2] + (img / 9 - 1) * g.per[2]};
+        dmin2 = fmin(dmin2, box_dist2(cc, g, q));
+      }
+      if (dmin2 < reach * reach) atomicMax(&rmax[q], __float_as_uint((float)(r * (1.0 + 1e-6))));
+    }
+  }
 }
 
 // records (receiver << 40 | decision << 32 | cell) and the next level's items
@@ -316,13 +349,32 @@ void let_setup(Ctx& c) {
   LetGeo g{};
   for (int a = 0; a < 3; ++a) { g.lo[a] = c.lo[a]; g.per[a] = c.per[a]; }
   g.L = c.L;
-  const double th = (double)c.cfg.theta_num / (double)c.cfg.theta_den;
-  g.coef = (3.0 + 2.0 * th) / th;
+  g.theta = (double)c.cfg.theta_num / (double)c.cfg.theta_den;
   g.leaf_first = c.cfg.traversal;
   for (int q = 0; q < P; ++q)
     for (int a = 0; a < 3; ++a) { g.blo[q][a] = boxes[7 * q + a]; g.bhi[q][a] = boxes[7 * q + 3 + a]; }
   LetCells lc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.leaf.p, c.cells.child_begin.p,
               c.cells.nchild.p, c.cells.count.p, c.cells.parent.p};
+  // every rank tells every other rank how large its leaves near that rank's domain are
+  {
+    c.dflag.reserve(std::max(8, P));
+    FMM_CUDA(cudaMemsetAsync(c.dflag.p, 0, sizeof(int) * P, st));
+    if (c.nleaves > 0)
+      FMM_LAUNCH(c, k_leaf_reach, grid_for(c.nleaves), 256, 0, c.leaf_ids.p, c.nleaves, lc, g, P, R,
+                 (unsigned*)c.dflag.p);
+    std::vector<unsigned> rm(P);
+    FMM_CUDA(cudaMemcpyAsync(rm.data(), c.dflag.p, sizeof(unsigned) * P, cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> send(P), got;
+    for (int q = 0; q < P; ++q) send[q] = (int64_t)rm[q];
+    got = alltoall_i64(c, send);
+    for (int q = 0; q < P; ++q) {
+      float f;
+      const unsigned u = (unsigned)got[q];
+      memcpy(&f, &u, 4);
+      g.rleaf[q] = q == R ? 0.0 : (double)f;
+    }
+  }
   // 1. the walk
   std::vector<uint64_t> seeds;
   if (n > 0)

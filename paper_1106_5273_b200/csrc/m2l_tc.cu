@@ -112,6 +112,7 @@ constexpr int kThreads = kRows + 32;
 // 3.4e-6; register kernel 4.8e-7, bar 1e-5)
 constexpr int kChunk = TC_CHUNK;
 constexpr int kMaxTcLevels = 16;
+constexpr int kMaxMapLevel = 8;             // forest source maps: 8^l entries per level, l <= 8
 
 // ---------------------------------------------------------------- PTX ----
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -218,7 +219,9 @@ __device__ __forceinline__ int tc_source(const TcGeo& g, int lt, const I (&ct)[3
     q[a] = (uint32_t)(((cs >> (kMaxLevel - ls)) - 1) >> 1);
   }
   const int m = (int)(spread3_32(q[0]) | (spread3_32(q[1]) << 1) | (spread3_32(q[2]) << 2));
-  return g.map ? __ldg(g.map + g.map_off[ls] + m) : g.lvl_begin[ls] + m;
+  if (!g.map) return g.lvl_begin[ls] + m;
+  const int off = g.map_off[ls];
+  return off < 0 ? -1 : __ldg(g.map + off + m);
 }
 
 // code of one M2L list entry (or -1 if outside the encodable range)
@@ -768,7 +771,7 @@ TcGeo make_geo(Ctx& c) {
   const int nl = (int)c.level_begin.size();
   for (int l = 0; l < kMaxLevel + 2; ++l) g.lvl_begin[l] = (int)c.level_begin[std::min(l, nl - 1)];
   g.map = c.cfg.nranks > 1 ? c.tc_map.p : nullptr;
-  for (int l = 0; l < kMaxLevel + 2; ++l) g.map_off[l] = l < (int)c.tc_map_off.size() ? (int)c.tc_map_off[l] : 0;
+  for (int l = 0; l < kMaxLevel + 2; ++l) g.map_off[l] = l < (int)c.tc_map_off.size() ? (int)c.tc_map_off[l] : -1;
   return g;
 }
 
@@ -799,19 +802,26 @@ void m2l_tc_prepare(Ctx& c) {
   c.tc_cq.reserve(std::max<int64_t>(c.ncells, 1));
   FMM_LAUNCH(c, k_tc_cq, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
              c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, c.tc_cq.p);
+  // candidate target levels: >= 1024 cells (smaller levels: the register kernel is as fast)
+  auto candidate = [&](int l) {
+    return l >= 2 && l < nlev && c.level_begin[l + 1] - c.level_begin[l] >= 1024 && (c.cfg.nranks == 1 || l + 1 <= kMaxMapLevel);
+  };
   if (c.cfg.nranks > 1) {
-    // LET forest: sources are found through a per-level map of all trees' cells
-    c.tc_map_off.assign(kMaxLevel + 2, 0);
+    // LET forest: sources are found through a per-level map of all trees' cells,
+    // built for the source levels (lt - 1, lt, lt + 1) of every candidate level;
+    // a level without a map makes tc_source return -1 (entry fails -> register kernel)
+    c.tc_map_off.assign(kMaxLevel + 2, -1);
     int64_t tot = 0;
-    for (int l = 2; l < nlev; ++l) {
-      c.tc_map_off[l] = tot;
-      if (c.level_begin[l + 1] - c.level_begin[l] >= 1024) tot += 1ll << (3 * l);
-    }
-    if (tot >= (1ll << 31) || tot == 0) return;
+    for (int l = 1; l <= kMaxMapLevel; ++l)
+      if (candidate(l - 1) || candidate(l) || candidate(l + 1)) {
+        c.tc_map_off[l] = tot;
+        tot += 1ll << (3 * l);
+      }
+    if (tot == 0) return;
     c.tc_map.reserve(std::max<int64_t>(tot, 1));
     FMM_LAUNCH(c, k_fill_i32, (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, c.tc_map.p, tot, -1);
-    for (int l = 2; l < nlev; ++l)
-      if (c.level_begin[l + 1] - c.level_begin[l] >= 1024)
+    for (int l = 1; l <= kMaxMapLevel; ++l)
+      if (c.tc_map_off[l] >= 0)
         FMM_LAUNCH(c, k_tc_map, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
                    c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, l, (int)c.tc_map_off[l], c.tc_map.p);
   }
@@ -833,8 +843,7 @@ void m2l_tc_prepare(Ctx& c) {
   const unsigned gl = (unsigned)std::min<int64_t>((c.nm2l + 255) / 256, 148 * 16);
   TcVer v{};
   for (int l = 2; l < nlev && v.nlv < kMaxTcLevels; ++l) {
-    const int lb = (int)c.level_begin[l], le = (int)c.level_begin[l + 1];
-    if (le - lb < 1024) continue;       // small levels: the register kernel is as fast
+    if (!candidate(l)) continue;
     if (first[l] == 0x7fffffff) continue;
     v.lt[v.nlv] = l;
     v.ref[v.nlv] = first[l];

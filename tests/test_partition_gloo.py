@@ -11,8 +11,9 @@ against the CPU oracle and numpy:
   along each cut.
 * LET completeness (let.cu): with Morton-octant ownership, every
   rank builds the oracle tree of ITS OWN particles, walks it against the other
-  rank's bounding box with the library's LET-MAC ((3 + 2 theta) r_B <
-  theta d_B over the first-layer images) and sends the cell tuples; the
+  rank's bounding box with the library's LET-MAC ((1 + theta) max(2 r_B,
+  rleaf) + r_B < theta d_B over the first-layer images, rleaf = the other
+  rank's largest leaf near this domain) and sends the cell tuples; the
   receiver checks, on the global tree's lists restricted to its own targets,
   that every remote M2L source is in the received LET and every remote P2P
   source leaf came with its bodies (so the remote branch of Alg. 2 is never
@@ -135,19 +136,35 @@ def _cell_geom(cells, lo, L):
     return c, s
 
 
-def _let_walk(cells, lo, L, box, theta, per):
+def _dmin(c, box, shifts):
+    cc = c[None, :] + shifts
+    d = np.maximum(0, np.maximum(box[0] - cc, cc - box[1]))
+    return np.sqrt((d * d).sum(1)).min()
+
+
+def _leaf_reach(cells, lo, L, box, theta, per):
+    """k_leaf_reach: the largest leaf radius that can meet a smaller cell of `box`."""
+    ctr, side = _cell_geom(cells, lo, L)
+    shifts = np.array([[(i % 3 - 1) * per, ((i // 3) % 3 - 1) * per, (i // 9 - 1) * per] for i in range(27)])
+    r = 0.8660254037844386 * side
+    best = 0.0
+    for c in np.nonzero(cells[:, 9])[0]:
+        if _dmin(ctr[c], box, shifts) < (1.5 / theta + 0.5) * r[c]:
+            best = max(best, r[c])
+    return best
+
+
+def _let_walk(cells, lo, L, box, theta, per, rleaf):
     """The LET-MAC walk of let.cu on an oracle tree: {(level, q): bodies?}."""
     ctr, side = _cell_geom(cells, lo, L)
-    coef = (3.0 + 2.0 * theta) / theta
     shifts = np.array([[(i % 3 - 1) * per, ((i // 3) % 3 - 1) * per, (i // 9 - 1) * per] for i in range(27)])
     out = {}
     stack = [0]
     while stack:
         c = stack.pop()
-        cc = ctr[c][None, :] + shifts
-        d = np.maximum(0, np.maximum(box[0] - cc, cc - box[1]))
-        dmin = np.sqrt((d * d).sum(1)).min()
-        acc = coef * 0.8660254037844386 * side[c] * (1 + 1e-9) < dmin
+        dmin = _dmin(ctr[c], box, shifts)
+        r = 0.8660254037844386 * side[c]
+        acc = ((1 + theta) * max(2 * r, rleaf) + r) / theta * (1 + 1e-9) < dmin
         key = tuple(int(v) for v in cells[c, :4])
         if cells[c, 9]:
             out[key] = not acc
@@ -174,7 +191,10 @@ def _let_worker(rank, world, port, q):
         box = np.array([x.min(0), x.max(0)], dtype=np.float64)
         boxes = [None] * world
         dist.all_gather_object(boxes, box)
-        lets = {r: _let_walk(cells_m, lo, L, boxes[r], theta, L) for r in range(world) if r != rank}
+        reach = {r: _leaf_reach(cells_m, lo, L, boxes[r], theta, L) for r in range(world) if r != rank}
+        reaches = [None] * world
+        dist.all_gather_object(reaches, reach)
+        lets = {r: _let_walk(cells_m, lo, L, boxes[r], theta, L, reaches[r][rank]) for r in range(world) if r != rank}
         got = [None] * world
         dist.all_gather_object(got, lets)
         recv = {}
