@@ -41,6 +41,15 @@ constexpr int TP = 64;           // targets per block pass and sources per tile
 constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
 constexpr float kFarRho2 = 4.6f * 4.6f;
 constexpr int kAdjChunk = 32;    // sources per FP32 partial for source leaves touching the target leaf
+#ifndef P2P_MINB
+#define P2P_MINB 16      // blocks (warps) per SM the launch bounds target
+#endif
+#ifndef P2P_UF
+#define P2P_UF 4         // unroll of the singular-branch loop
+#endif
+#ifndef P2P_UN
+#define P2P_UN 4         // unroll of the regularised-branch loop
+#endif
 #ifndef P2P_ADJ_MODE
 #define P2P_ADJ_MODE 1
 #endif   // rho^2 at and beyond which the singular branch is exact to Z6
@@ -517,11 +526,11 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near, int part) {
   const int* sb = part == 2 ? c.p2p_m.p : c.p2p_b.p;
   const int* se = part == 1 ? c.p2p_m.p : c.p2p_e.p;
   if (part == 2)
-    FMM_LAUNCH(c, (k_p2p<16, 4, 4, true>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
+    FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, true>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
                c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
                c.dnear.p);
   else
-    FMM_LAUNCH(c, (k_p2p<16, 4, 4, false>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
+    FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, false>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
                c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
                c.dnear.p);
 }
