@@ -21,8 +21,8 @@ struct Cells {
 
 // a level whose cells all take the tensor-core M2L (m2l_tc.cu)
 struct TcLevel {
-  int lt = 0, D = 0, ntgt = 0;
-  int64_t tgt_off = 0, code_off = 0, op_off = 0;
+  int lt = 0, D = 0, ntgt = 0, lb = 0, W = 0;
+  int64_t tgt_off = 0, code_off = 0, op_off = 0, mask_off = 0;
 };
 
 enum Phase { PH_SET0, PH_KEYS, PH_SORT, PH_TREE, PH_EVAL0, PH_UP, PH_TRAV, PH_M2L, PH_P2P, PH_DOWN, PH_FIN, PH_N };
@@ -124,6 +124,7 @@ struct Ctx {
   int64_t nm2lr = 0;
   DBuf<int> dsel;                            // selected-count output of cub::DeviceSelect
   DBuf<unsigned> tc_mask;                    // tensor-path verification: offset bitmask per cell
+  DBuf<unsigned> tc_good, tc_hist;           // per M2L entry: taken by the tensor path (bit); offset histogram
   DBuf<unsigned char> tc_bad, tc_has;        // tc_has[t]: cell t has M2L entries (written by the traversal)
   DBuf<int64_t> tc_off;
   DBuf<int4> tc_cq;                          // packed (qx, qy, qz, level) for the verification

@@ -349,85 +349,114 @@ __device__ __forceinline__ int ver_level(const TcVer& v, int t) {
   return -1;
 }
 
-// first cell of [lb, le) with M2L entries (has[] is written by the traversal)
-__global__ void k_tc_first(const unsigned char* __restrict__ has, int lb, int le, int* __restrict__ out) {
-  for (int c = lb + blockIdx.x * blockDim.x + threadIdx.x; c < le; c += gridDim.x * blockDim.x)
-    if (has[c]) {
-      atomicMin(out, c);
-      return;                    // later cells of this thread are larger
-    }
-}
-
-// the reference cells' entries as offset codes (appended per level; the
-// order is irrelevant, the host sorts them)
-__global__ void k_tc_ref_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g, int cap,
-                                 int* __restrict__ codes, int* __restrict__ cnt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t ent = lst[i];
-    const int t = (int)(ent >> 32);
-    for (int k = 0; k < v.nlv; ++k) {
-      if (t != v.ref[k]) continue;
-      long long ct[3];
-      centre(g, t, v.lt[k], ct);
-      const int j = atomicAdd(&cnt[k], 1);
-      if (j < cap) codes[(int64_t)k * cap + j] = entry_code(g, v.lt[k], ct, ent);
-    }
-  }
-}
-
-// per entry whose target is in a candidate level: its offset, reflected into
-// class 0, is in the canonical table and its source is the one tc_source
-// computes; the offset's bit is set in the target's mask (a bit already set
-// is a duplicate).  Any failure marks the target bad.
-__global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
-                                    const short* __restrict__ tbl, unsigned* __restrict__ mask,
-                                    unsigned char* __restrict__ bad) {
+// offset histogram per candidate level: every entry's offset code, reflected
+// into class 0, counted in a dense (dl, v) table of half-width kHR; the
+// level's canonical set is then the codes a majority of its cells use
+constexpr int kHR = 24;                 // |v| <= 24 finest-level units: covers the theta = 1/2 lists
+constexpr int kHV = 2 * kHR + 1;
+constexpr int kHBins = 3 * kHV * kHV * kHV;
+constexpr int kHSample = 16;             // the histogram samples every 16th cell (163M atomics on ~550 bins otherwise)
+__global__ void k_tc_code_hist(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
+                               unsigned* __restrict__ hist) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t ent = lst[i];
     const int t = (int)(ent >> 32);
     const int k = ver_level(v, t);
     if (k < 0) continue;
-    const int lt = v.lt[k], R = v.R[k], V = 2 * R + 1;
+    const int lt = v.lt[k];
+    if ((t - v.lb[k]) & (kHSample - 1)) continue;     // every kHSample-th cell of the level
     const int4 tq = __ldg(g.cq + t);
     long long ct[3];
     ct[0] = (long long)(2 * tq.x + 1) << (kMaxLevel - lt);
     ct[1] = (long long)(2 * tq.y + 1) << (kMaxLevel - lt);
     ct[2] = (long long)(2 * tq.z + 1) << (kMaxLevel - lt);
     const int code = entry_code4(g, lt, ct, ent);
-    bool good = code >= 0;
-    int d = -1;
-    if (good) {
-      const int c0 = reflect(code, (tq.x & 1) | ((tq.y & 1) << 1) | ((tq.z & 1) << 2));
-      const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
-      good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
-      if (good) d = tbl[v.tbl_off[k] + (((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R];
-      good = good && d >= 0;
-    }
-    if (good) good = tc_source(g, lt, ct, code) == (int)((ent >> 5) & 0x7ffffff);
-    const int64_t row = (int64_t)(t - v.lb[k]);
-    if (good) {
-      const unsigned bit = 1u << (d & 31);
-      const unsigned old = atomicOr(&mask[v.mask_off[k] + row * v.W[k] + (d >> 5)], bit);
-      good = !(old & bit);
-    }
-    if (!good) bad[v.lb[k] + row] = 1;
+    if (code < 0) continue;
+    const int c0 = reflect(code, (tq.x & 1) | ((tq.y & 1) << 1) | ((tq.z & 1) << 2));
+    const int vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
+    if (vx < -kHR || vx > kHR || vy < -kHR || vy > kHR || vz < -kHR || vz > kHR) continue;
+    atomicAdd(&hist[(int64_t)k * kHBins + (((code_dl(c0) + 1) * kHV + vx + kHR) * kHV + vy + kHR) * kHV + vz + kHR], 1u);
   }
 }
 
-// per cell of the candidate levels: all D canonical offsets present exactly
-// once and no bad entry -> taken by the tensor path (appended per level)
+__global__ void k_tc_count_has(const unsigned char* __restrict__ has, TcVer v, int* __restrict__ cnt) {
+  for (int k = 0; k < v.nlv; ++k) {
+    int m = 0;
+    for (int c = v.lb[k] + (int)(blockIdx.x * blockDim.x + threadIdx.x); c < v.le[k]; c += (int)(gridDim.x * blockDim.x))
+      m += (has[c] && !((c - v.lb[k]) & (kHSample - 1))) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&cnt[k], m);
+  }
+}
+
+// per entry whose target is in a candidate level: its offset, reflected into
+// class 0, is in the canonical table and its source is the one tc_source
+// computes -> the entry is "good" (bit i of the per-entry words: the tensor
+// path may take it) and its offset's bit is set in the target's mask; a bit
+// already set is a duplicate (the target then stays off the tensor path).
+// Other entries of a target (offsets outside the level's canonical set, or a
+// source elsewhere than the canonical cell: adaptive trees) stay on the
+// register kernel, whichever path takes the target's canonical ones.
+__global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
+                                    const short* __restrict__ tbl, unsigned* __restrict__ mask,
+                                    unsigned char* __restrict__ bad, unsigned* __restrict__ goodw) {
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + (threadIdx.x & 31);
+    bool good = false;
+    if (i < n) {
+      const uint64_t ent = lst[i];
+      const int t = (int)(ent >> 32);
+      const int k = ver_level(v, t);
+      if (k >= 0) {
+        const int lt = v.lt[k], R = v.R[k], V = 2 * R + 1;
+        const int4 tq = __ldg(g.cq + t);
+        long long ct[3];
+        ct[0] = (long long)(2 * tq.x + 1) << (kMaxLevel - lt);
+        ct[1] = (long long)(2 * tq.y + 1) << (kMaxLevel - lt);
+        ct[2] = (long long)(2 * tq.z + 1) << (kMaxLevel - lt);
+        const int code = entry_code4(g, lt, ct, ent);
+        good = code >= 0;
+        int d = -1;
+        if (good) {
+          const int c0 = reflect(code, (tq.x & 1) | ((tq.y & 1) << 1) | ((tq.z & 1) << 2));
+          const int dl = code_dl(c0), vx = code_v(c0, 0), vy = code_v(c0, 1), vz = code_v(c0, 2);
+          good = vx >= -R && vx <= R && vy >= -R && vy <= R && vz >= -R && vz <= R;
+          if (good) d = tbl[v.tbl_off[k] + (((dl + 1) * V + vx + R) * V + vy + R) * V + vz + R];
+          good = good && d >= 0;
+        }
+        if (good) good = tc_source(g, lt, ct, code) == (int)((ent >> 5) & 0x7ffffff);
+        if (good) {
+          const int64_t row = (int64_t)(t - v.lb[k]);
+          const unsigned bit = 1u << (d & 31);
+          const unsigned old = atomicOr(&mask[v.mask_off[k] + row * v.W[k] + (d >> 5)], bit);
+          if (old & bit) bad[v.lb[k] + row] = 1;
+        }
+      }
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, good);
+    if ((threadIdx.x & 31) == 0 && i0 < n) goodw[i0 >> 5] = w;
+  }
+}
+
+// per cell of the candidate levels: no duplicate and at least kMinFrac of the
+// D canonical offsets present -> taken by the tensor path (appended per level;
+// its missing offsets are masked to zero rows in the kernel, and its
+// remaining entries stay on the register kernel)
+constexpr float kMinFrac = 0.4f;
 __global__ void k_tc_accept(TcVer v, const unsigned* __restrict__ mask, const unsigned char* __restrict__ bad,
                             unsigned char* __restrict__ skip, int* __restrict__ tgt, const int64_t* __restrict__ tgt_off,
-                            int* __restrict__ ntgt) {
+                            int* __restrict__ ntgt, unsigned long long* __restrict__ nent) {
   for (int k = 0; k < v.nlv; ++k) {
     for (int c = v.lb[k] + (int)(blockIdx.x * blockDim.x + threadIdx.x); c < v.le[k]; c += (int)(gridDim.x * blockDim.x)) {
       if (bad[c]) continue;
       int pc = 0;
       const unsigned* m = mask + v.mask_off[k] + (int64_t)(c - v.lb[k]) * v.W[k];
       for (int w = 0; w < v.W[k]; ++w) pc += __popc(m[w]);
-      if (pc == v.D[k]) {
-        skip[c] = 1;
+      if (pc > 0 && (float)pc >= kMinFrac * (float)v.D[k]) {
+        skip[c] = pc == v.D[k] ? 1 : 2;          // 1: every canonical offset (no mask lookups), 2: masked
         tgt[tgt_off[k] + atomicAdd(&ntgt[k], 1)] = c;
+        atomicAdd(nent, (unsigned long long)pc);
       }
     }
   }
@@ -536,7 +565,9 @@ struct TcLevelArg {
   const int* tgt;
   const int* codes;
   const unsigned char* op;
-  int ntgt, lt, D, cta_begin;
+  const unsigned* mask;          // per target cell (cell - lb) x W words: canonical offsets present
+  const unsigned char* skip;     // per cell: 1 = every canonical offset, 2 = subset (mask)
+  int ntgt, lt, D, cta_begin, lb, W;
 };
 struct TcArgs {
   TcLevelArg lv[kMaxTcLevels];
@@ -584,11 +615,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
     int ct[3];
     int comp, cls;
     const float* src = (const float*)Mp;
+    const unsigned* mrow;
+    bool on = false;                       // the row's target has the current offset
+    bool allon = true;                     // ... every canonical offset (no mask lookups)
     {
       const int R = row0 + tid;
       const int t = R < 3 * A.ntgt ? R / 3 : 0;
       comp = R < 3 * A.ntgt ? R - 3 * (R / 3) : 0;
       const int cell = A.tgt[t];
+      mrow = A.mask + (size_t)(cell - A.lb) * A.W;
+      allon = A.skip[cell] == 1;
       cls = parity_class(g, cell);
       ct[0] = (2 * g.qx[cell] + 1) << (kMaxLevel - A.lt);
       ct[1] = (2 * g.qy[cell] + 1) << (kMaxLevel - A.lt);
@@ -599,13 +635,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
       const int d = it / kSPO, kb = (it - kSPO * (it / kSPO)) * kKPS;
       if (d != pf_d) {
         pf_d = d;
-        const int code = __ldg(A.codes + d);
+        on = allon || ((__ldg(mrow + (d >> 5)) >> (d & 31)) & 1u);
+        if (on) {
+          const int code = __ldg(A.codes + d);
 #if TC_DIAG == 1
-        const int s = A.tgt[(row0 + tid) < 3 * A.ntgt ? (row0 + tid) / 3 : 0] + 0 * code;   // diagnostic: no gather spread
+          const int s = A.tgt[(row0 + tid) < 3 * A.ntgt ? (row0 + tid) / 3 : 0] + 0 * code;   // diagnostic: no gather spread
 #else
-        const int s = tc_source(g, A.lt, ct, reflect(code, cls));
+          const int s = tc_source(g, A.lt, ct, reflect(code, cls));
 #endif
-        src = (const float*)Mp + ((size_t)s * kNKB * kMpLine + comp * 2) * 4;
+          src = (const float*)Mp + ((size_t)s * kNKB * kMpLine + comp * 2) * 4;
+        }
+      }
+      if (!on) {                                   // offset absent from the target's list: zero row
+#pragma unroll
+        for (int q = 0; q < 8 * kKPS; ++q) v[q] = 0.f;
+        return;
       }
 #if TC_DIAG == 2
       for (int q = 0; q < 8 * kKPS; ++q) v[q] = __int_as_float(kb + q);   // diagnostic: no loads
@@ -830,62 +874,52 @@ void m2l_tc_prepare(Ctx& c) {
   cudaStream_t st = c.stream;
   struct Cand { int lt, D, R; std::vector<int> codes; std::vector<short> tbl; };
   std::vector<Cand> cands;
-  // the first cell with M2L entries in every level (the reference cells)
-  std::vector<int> first(kMaxLevel + 2, 0x7fffffff);
-  c.tc_tmp.reserve(kMaxLevel + 2);
-  FMM_CUDA(cudaMemcpyAsync(c.tc_tmp.p, first.data(), sizeof(int) * first.size(), cudaMemcpyHostToDevice, st));
-  for (int l = 2; l < nlev; ++l) {
-    const int lb = (int)c.level_begin[l], le = (int)c.level_begin[l + 1];
-    if (le - lb >= 1024) FMM_LAUNCH(c, k_tc_first, 148, 256, 0, c.tc_has.p, lb, le, c.tc_tmp.p + l);
-  }
-  FMM_CUDA(cudaMemcpyAsync(first.data(), c.tc_tmp.p, sizeof(int) * first.size(), cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaStreamSynchronize(st));
   const unsigned gl = (unsigned)std::min<int64_t>((c.nm2l + 255) / 256, 148 * 16);
   TcVer v{};
   for (int l = 2; l < nlev && v.nlv < kMaxTcLevels; ++l) {
     if (!candidate(l)) continue;
-    if (first[l] == 0x7fffffff) continue;
     v.lt[v.nlv] = l;
-    v.ref[v.nlv] = first[l];
+    v.lb[v.nlv] = (int)c.level_begin[l];
+    v.le[v.nlv] = (int)c.level_begin[l + 1];
     ++v.nlv;
   }
   if (v.nlv == 0) return;
-  // one pass: the reference cells' offset codes
-  constexpr int kCap = 8192;
-  c.tc_codes_tmp.reserve((int64_t)kCap * v.nlv);
+  // one pass: the histogram of every level's offsets (class 0) and its cells with entries
+  c.tc_hist.reserve((int64_t)kHBins * v.nlv);
   c.tc_cnt.reserve(kMaxTcLevels);
+  FMM_CUDA(cudaMemsetAsync(c.tc_hist.p, 0, sizeof(unsigned) * kHBins * v.nlv, st));
   FMM_CUDA(cudaMemsetAsync(c.tc_cnt.p, 0, sizeof(int) * kMaxTcLevels, st));
-  FMM_LAUNCH(c, k_tc_ref_entries, gl, 256, 0, c.m2l.p, c.nm2l, v, g, kCap, c.tc_codes_tmp.p, c.tc_cnt.p);
-  std::vector<int> rcnt(kMaxTcLevels);
-  std::vector<int> rcodes((size_t)kCap * v.nlv);
-  FMM_CUDA(cudaMemcpyAsync(rcnt.data(), c.tc_cnt.p, sizeof(int) * kMaxTcLevels, cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaMemcpyAsync(rcodes.data(), c.tc_codes_tmp.p, sizeof(int) * rcodes.size(), cudaMemcpyDeviceToHost, st));
+  FMM_LAUNCH(c, k_tc_code_hist, gl, 256, 0, c.m2l.p, c.nm2l, v, g, c.tc_hist.p);
+  FMM_LAUNCH(c, k_tc_count_has, 148 * 4, 256, 0, c.tc_has.p, v, c.tc_cnt.p);
+  std::vector<unsigned> hist((size_t)kHBins * v.nlv);
+  std::vector<int> nhas(kMaxTcLevels);
+  FMM_CUDA(cudaMemcpyAsync(hist.data(), c.tc_hist.p, sizeof(unsigned) * hist.size(), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(nhas.data(), c.tc_cnt.p, sizeof(int) * kMaxTcLevels, cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
   for (int k = 0; k < v.nlv; ++k) {
-    const int l = v.lt[k], ref = v.ref[k], D = rcnt[k];
-    if (D <= 0 || D > kCap) continue;
-    int hq[3] = {0, 0, 0};
-    FMM_CUDA(cudaMemcpyAsync(&hq[0], c.cells.qx.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaMemcpyAsync(&hq[1], c.cells.qy.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaMemcpyAsync(&hq[2], c.cells.qz.p + ref, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMM_CUDA(cudaStreamSynchronize(st));
+    const int l = v.lt[k];
+    if (nhas[k] <= 0) continue;
+    // canonical (class 0) offsets: those a majority of the level's cells with entries use
+    // (all of them, each exactly once per cell, on a uniform level)
     Cand cd;
     cd.lt = l;
-    cd.D = D;
-    cd.codes.assign(rcodes.begin() + (size_t)k * kCap, rcodes.begin() + (size_t)k * kCap + D);
-    if (*std::min_element(cd.codes.begin(), cd.codes.end()) < 0) continue;
-    // canonical (class 0) offsets: the reference cell's, reflected from its class
-    const int rcls = (hq[0] & 1) | ((hq[1] & 1) << 1) | ((hq[2] & 1) << 2);
-    for (int& code : cd.codes) code = reflect(code, rcls);
+    for (int dl = -1; dl <= 1; ++dl)
+      for (int x = -kHR; x <= kHR; ++x)
+        for (int y = -kHR; y <= kHR; ++y)
+          for (int z = -kHR; z <= kHR; ++z) {
+            const unsigned h = hist[(size_t)k * kHBins + (((dl + 1) * kHV + x + kHR) * kHV + y + kHR) * kHV + z + kHR];
+            if (2ll * h > (long long)nhas[k]) cd.codes.push_back(((dl + 1) << 21) | ((x + 64) << 14) | ((y + 64) << 7) | (z + 64));
+          }
+    cd.D = (int)cd.codes.size();
+    if (cd.D == 0) continue;
     std::sort(cd.codes.begin(), cd.codes.end());
-    if (std::adjacent_find(cd.codes.begin(), cd.codes.end()) != cd.codes.end()) continue;
     int R = 0;
     for (int code : cd.codes)
       for (int a = 0; a < 3; ++a) R = std::max(R, std::abs(code_v(code, a)));
     const int V = 2 * R + 1;
     cd.R = R;
     cd.tbl.assign((size_t)3 * V * V * V, (short)-1);
-    for (int d = 0; d < D; ++d) {
+    for (int d = 0; d < cd.D; ++d) {
       const int code = cd.codes[d];
       cd.tbl[(((size_t)(code_dl(code) + 1) * V + code_v(code, 0) + R) * V + code_v(code, 1) + R) * V +
              code_v(code, 2) + R] = (short)d;
@@ -929,12 +963,19 @@ void m2l_tc_prepare(Ctx& c) {
   }
   c.tc_off.reserve(kMaxTcLevels);
   FMM_CUDA(cudaMemcpyAsync(c.tc_off.p, tgt_off.data(), sizeof(int64_t) * tgt_off.size(), cudaMemcpyHostToDevice, st));
-  FMM_LAUNCH(c, k_tc_verify_entries, gl, 256, 0, c.m2l.p, c.nm2l, w, g, c.tc_tbl.p, c.tc_mask.p, c.tc_bad.p);
+  c.tc_good.reserve((c.nm2l + 31) / 32 + 1);
+  FMM_CUDA(cudaMemsetAsync(c.tc_good.p, 0, sizeof(unsigned) * ((c.nm2l + 31) / 32 + 1), st));
+  c.dcount.reserve(1);
+  FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
+  FMM_LAUNCH(c, k_tc_verify_entries, gl, 256, 0, c.m2l.p, c.nm2l, w, g, c.tc_tbl.p, c.tc_mask.p, c.tc_bad.p,
+             c.tc_good.p);
   FMM_LAUNCH(c, k_tc_accept, 148 * 4, 256, 0, w, c.tc_mask.p, c.tc_bad.p, c.tc_skip.p, c.tc_tgt.p, c.tc_off.p,
-             c.tc_cnt.p);
+             c.tc_cnt.p, c.dcount.p);
   FMM_CUDA(cudaStreamSynchronize(st));    // host vectors above are read by the copies
   std::vector<int> cnt(cands.size());
+  unsigned long long nent = 0;
   FMM_CUDA(cudaMemcpyAsync(cnt.data(), c.tc_cnt.p, sizeof(int) * cands.size(), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(&nent, c.dcount.p, sizeof(nent), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
   // Morton order of the targets (= cell index order within a level)
   for (size_t i = 0; i < cands.size(); ++i) {
@@ -977,9 +1018,12 @@ void m2l_tc_prepare(Ctx& c) {
     tl.tgt_off = tgt_off[i];
     tl.code_off = code_off[i];
     tl.op_off = op_off[i];
+    tl.mask_off = w.mask_off[i];
+    tl.lb = w.lb[i];
+    tl.W = w.W[i];
     c.tc_levels.push_back(tl);
-    c.tc_entries += (int64_t)cnt[i] * cands[i].D;
   }
+  c.tc_entries = (int64_t)nent;           // the entries the tensor path evaluates (masked rows excluded)
   // longest CTAs first
   std::sort(c.tc_levels.begin(), c.tc_levels.end(), [](const TcLevel& a, const TcLevel& b) { return a.D > b.D; });
 }
@@ -1003,8 +1047,8 @@ void m2l_tc_run(Ctx& c) {
     args.nlv = (int)std::min<size_t>(kMaxTcLevels, c.tc_levels.size() - g0);
     for (int i = 0; i < args.nlv; ++i) {
       const TcLevel& tl = c.tc_levels[g0 + i];
-      args.lv[i] = {c.tc_tgt2.p + tl.tgt_off, c.tc_codes.p + tl.code_off, c.tc_op.p + tl.op_off, tl.ntgt, tl.lt, tl.D,
-                    ctas};
+      args.lv[i] = {c.tc_tgt2.p + tl.tgt_off, c.tc_codes.p + tl.code_off, c.tc_op.p + tl.op_off,
+                    c.tc_mask.p + tl.mask_off, c.tc_skip.p, tl.ntgt, tl.lt, tl.D, ctas, tl.lb, tl.W};
       ctas += (int)((3 * (int64_t)tl.ntgt + kRows - 1) / kRows);
     }
     FMM_LAUNCH(c, k_m2l_tc, (unsigned)ctas, kThreads, smem, args, T, g, (const float4*)c.tc_mp.p, c.Lc.p);

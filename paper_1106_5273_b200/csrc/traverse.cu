@@ -177,13 +177,20 @@ void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
 
 }  // namespace
 
-struct NotOnTensorPath {
+// entry i stays on the register kernel unless its target is on the tensor path
+// and the tensor path verified this entry (m2l_tc_prepare's per-entry bits)
+struct OnRegisterPath {
+  const uint64_t* lst;
   const unsigned char* skip;
-  __device__ __forceinline__ bool operator()(const uint64_t& e) const { return !skip[(int)(e >> 32)]; }
+  const unsigned* good;
+  __device__ __forceinline__ char operator()(const int64_t& i) const {
+    if (!skip[(int)(lst[i] >> 32)]) return 1;
+    return ((good[i >> 5] >> (i & 31)) & 1u) ? 0 : 1;
+  }
 };
 
-// the M2L entries whose target the tensor path did not take (tc_skip == 0),
-// in emission order (stable select), grouped by target (stable sort), with
+// the M2L entries the tensor path does not take (target not taken, or entry
+// not verified), in emission order (stable select), grouped by target (stable sort), with
 // per-target segments m2l_b/m2l_e for the register kernels
 void m2l_reg_segments(Ctx& c) {
   cudaStream_t st = c.stream;
@@ -197,9 +204,11 @@ void m2l_reg_segments(Ctx& c) {
   uint64_t* out = c.m2lr.p;
   int* nsel = c.dsel.p;
   const int n = (int)c.nm2l;
-  NotOnTensorPath pred{c.tc_skip.p};
+  cub::CountingInputIterator<int64_t> idx(0);
+  cub::TransformInputIterator<char, OnRegisterPath, cub::CountingInputIterator<int64_t>> flags(
+      idx, OnRegisterPath{c.m2l.p, c.tc_skip.p, c.tc_good.p});
   cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceSelect::If(tmp, bytes, in, out, nsel, n, pred, st);
+    return cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, nsel, n, st);
   });
   int ns = 0;
   FMM_CUDA(cudaMemcpyAsync(&ns, c.dsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
