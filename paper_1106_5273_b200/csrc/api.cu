@@ -148,16 +148,44 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
     FMM_CUDA(cudaStreamWaitEvent(st, c.ev_let1, 0));
   }
   FMM_CUDA(cudaStreamWaitEvent(st, c.ev[PH_UP], 0));
-  FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));     // (multi: start of the part after the LET)
-  // a9 M2L + a8 periodic far layers
-  FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
-  m2l_pass(c);
-  periodic_far_pass(c);
-  FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
-  // a12 (multi: the received sources' entries, added)
-  p2p_pass(c, c.u_near.p, c.s_near.p, multi ? 2 : 0);
-  FMM_CUDA(cudaEventRecord(c.ev[PH_N], st));
   cudaEvent_t ev_p2p_end = c.ev[PH_N];
+  const int conc = multi ? 0 : c.concurrent;
+  if (conc == 0) {
+    FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));     // (multi: start of the part after the LET)
+    // a9 M2L + a8 periodic far layers
+    FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
+    m2l_pass(c);
+    periodic_far_pass(c);
+    FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
+    // a12 (multi: the received sources' entries, added)
+    p2p_pass(c, c.u_near.p, c.s_near.p, multi ? 2 : 0);
+    FMM_CUDA(cudaEventRecord(c.ev[PH_N], st));
+  } else {
+    // the far field (a8-a9, tensor and CUDA cores) and the near field (a12, FP32
+    // pipe) are independent: M2L on the high-priority side stream beside P2P
+    FMM_CUDA(cudaEventRecord(c.ev_fork, st));
+    FMM_CUDA(cudaStreamWaitEvent(c.mstream, c.ev_fork, 0));
+    auto near = [&] {
+      FMM_CUDA(cudaEventRecord(c.ev[PH_TRAV], st));
+      p2p_pass(c, c.u_near.p, c.s_near.p, 0);
+      FMM_CUDA(cudaEventRecord(c.ev[PH_N], st));
+    };
+    if (conc == 1) near();
+    std::swap(c.stream, c.mstream);
+    try {
+      FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], c.stream));
+      FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), c.stream));
+      m2l_pass(c);
+      periodic_far_pass(c);
+      FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], c.stream));
+    } catch (...) {
+      std::swap(c.stream, c.mstream);
+      throw;
+    }
+    std::swap(c.stream, c.mstream);
+    if (conc == 2) near();
+    FMM_CUDA(cudaStreamWaitEvent(st, c.ev[PH_M2L], 0));
+  }
   // a10-a11 downward pass
   downward_pass(c, c.u_far.p, c.s_far.p);
   FMM_CUDA(cudaEventRecord(c.ev[PH_DOWN], st));
@@ -195,14 +223,14 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   // overlapped: both phases start at EVAL0 (ms_upward and ms_traverse then overlap in time)
   S.ms_traverse = c.overlapped ? ms_between(c.ev[PH_EVAL0], c.ev_trav) : 0.0;
   S.ms_m2l = ms_between(c.ev[PH_P2P], c.ev[PH_M2L]);
-  S.ms_p2p = ms_between(c.ev[PH_M2L], ev_p2p_end);
+  S.ms_p2p = conc ? ms_between(c.ev[PH_TRAV], ev_p2p_end) : ms_between(c.ev[PH_M2L], ev_p2p_end);
   if (multi) {
     S.ms_p2p += ms_between(c.ev[PH_TRAV], c.ev_p2p_loc);
     c.ms_let = ms_between(c.ev_let0, c.ev_let1);
     // time the main stream waited for the LET after its local near field
     c.ms_let_exposed = std::max(0.0, (double)ms_between(c.ev_p2p_loc, c.ev[PH_P2P]));
   }
-  S.ms_downward = ms_between(ev_p2p_end, c.ev[PH_DOWN]);
+  S.ms_downward = conc ? 0.0 : ms_between(ev_p2p_end, c.ev[PH_DOWN]);
   S.ms_finalize = ms_between(c.ev[PH_DOWN], c.ev[PH_FIN]);
   S.ms_eval_total = ms_between(c.ev[PH_EVAL0], c.ev[PH_FIN]);
   S.ms_m2l_tc = c.nm2l ? ms_between(c.ev_m2l[0], c.ev_m2l[1]) : 0.0;
@@ -267,6 +295,13 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     for (int i = 0; i <= PH_N; ++i) FMM_CUDA(cudaEventCreate(&c.ev[i]));
     // side stream: the upward pass runs beside the traversal (they are independent)
     FMM_CUDA(cudaStreamCreateWithFlags(&c.stream2, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      FMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      FMM_CUDA(cudaStreamCreateWithPriority(&c.mstream, cudaStreamNonBlocking, hi));
+      const char* e = getenv("FMM_CONCURRENT");
+      c.concurrent = e ? atoi(e) : 0;
+    }
     if (cfg->nranks > 1) {
       FMM_CUDA(cudaStreamCreateWithFlags(&c.cstream, cudaStreamNonBlocking));
       for (cudaEvent_t* e : {&c.ev_let0, &c.ev_let1, &c.ev_p2p_loc}) FMM_CUDA(cudaEventCreate(e));
@@ -290,6 +325,7 @@ FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.stream2) cudaStreamSynchronize(c.stream2);
   if (c.cstream) cudaStreamSynchronize(c.cstream);
+  if (c.mstream) { cudaStreamSynchronize(c.mstream); cudaStreamDestroy(c.mstream); }
   for (cudaEvent_t e : {c.ev_let0, c.ev_let1, c.ev_p2p_loc}) if (e) cudaEventDestroy(e);
   if (c.cstream) cudaStreamDestroy(c.cstream);
   for (int i = 0; i <= PH_N; ++i) if (c.ev[i]) cudaEventDestroy(c.ev[i]);

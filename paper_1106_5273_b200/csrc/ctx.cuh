@@ -50,6 +50,8 @@ struct Ctx {
   fmm_config cfg{};
   int P = 10, nc = 55;
   cudaStream_t stream = nullptr, stream2 = nullptr;
+  cudaStream_t mstream = nullptr;            // far field beside the near field (high priority)
+  int concurrent = 0;                        // 0: M2L then P2P; 1: P2P first, M2L beside; 2: M2L first, P2P beside
   bool own_stream = false;
   std::string err;
   bool poisoned = false;

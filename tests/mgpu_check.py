@@ -73,7 +73,8 @@ def rel(p, q):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=16)
-    ap.add_argument("--mode", choices=["tiled", "refined", "orb", "orb_cloud", "step"], default="tiled")
+    ap.add_argument("--mode", choices=["tiled", "refined", "orb", "orb_cloud", "step", "uneven", "leaf_first"],
+                    default="tiled")
     args = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -91,12 +92,21 @@ def main():
         gen = lambda side, w, r: tuple(v[synth.scatter_to_ranks(len(full[0]), w, r)] for v in full)
     elif args.mode == "tiled":
         gen = synth.taylor_green_tile
+    elif args.mode == "uneven":
+        # partition 0 with an arbitrary split: rank 0 holds nothing, the others a jittered
+        # lattice cut at uneven x positions (no octant alignment)
+        full = synth.jittered_lattice(args.side)
+        order = np.argsort(full[0][:, 0], kind="stable")
+        cuts = np.linspace(0, len(order), world + 1).astype(int)
+        cuts[1] = 0                                   # rank 0: empty
+        gen = lambda side, w, r: tuple(v[np.sort(order[cuts[r]:cuts[r + 1]])] for v in full)
     else:
         gen = synth.taylor_green_octants
     tiles = synth.RANK_TILES[world] if args.mode == "tiled" else (1, 1, 1)
     x, a, s = gen(args.side, world, rank)
+    trav = 1 if args.mode == "leaf_first" else 0
     fmm = P.FMM(images=images, nranks=world, rank=rank, device=local, nccl_id=obj[0], tiles=tiles,
-                partition=1 if orb else 0)
+                partition=1 if orb else 0, traversal=trav)
     res = {}
     if args.mode == "step":
         dt = 0.5 * float(s[0])
@@ -121,7 +131,7 @@ def main():
         S = np.concatenate([b[2] for b in blocks])
         msg["fallback"] = [int(g["stats"]["let_fallback"]) for g in gathered]
         ok &= all(f == 0 for f in msg["fallback"])
-        single = P.FMM(images=images, device=local, tiles=tiles)
+        single = P.FMM(images=images, device=local, tiles=tiles, traversal=trav)
         if args.mode == "step":
             dt = 0.5 * float(S[0])
             xs, as_, ss = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (X, A, S))
@@ -142,7 +152,7 @@ def main():
             U, SS = run(single, X, A, S)
             gp2p, gm2l = P.fmm_get_lists(single.ctx)
             gcells = P.fmm_get_cells(single.ctx)
-            if args.mode in ("tiled", "refined"):
+            if args.mode in ("tiled", "refined", "leaf_first"):
                 for r in range(world):
                     g = gathered[r]
                     nloc = g["stats"]["ncells_local"]
@@ -178,12 +188,13 @@ def main():
                 msg["full_vs_direct"] = [rel(DU, u0), rel(DS, s0)]
                 msg["single_vs_direct"] = [rel(U, u0), rel(SS, s0)]
                 ok &= max(msg["full_vs_direct"]) <= 1e-3 and max(msg["full_vs_single"]) <= 1e-3
-            elif orb:
-                # ORB cuts need not fall on cell boundaries (3 ranks): the near/far split then
+            elif orb or args.mode == "uneven":
+                # ORB / uneven cuts need not fall on cell boundaries: the near/far split then
                 # differs from the single-GPU tree's and only the full field is comparable
                 ok &= max(msg["full_vs_single"]) <= 1e-4
             else:
                 ok &= max(msg["near_vs_single"]) <= 2e-6 and max(msg["full_vs_single"]) <= 1e-5
+            if args.mode in ("tiled", "refined", "leaf_first", "orb"):
                 uc, sc = tg_closed(X, A, S[0])
                 msg["closed_form"] = [rel(DU, uc), rel(DS, sc)]
                 ok &= max(msg["closed_form"]) <= 1e-3

@@ -58,3 +58,14 @@ def test_multi_gpu_time_step(world):
     if _ngpu() < world:
         pytest.skip("needs %d GPUs" % world)
     _launch(world, "step", 16, 29540 + world)
+
+
+@pytest.mark.parametrize("mode", ["uneven", "leaf_first"])
+def test_let_forest_edge_cases(mode):
+    """a14 edge cases on 2 GPUs: a rank with no particles and uneven cuts through
+    cells (partition 0, jittered lattice), and the leaf-first traversal (Z11)
+    whose LET carries the bodies of every visited leaf; fallback 0, full field
+    against one GPU and the closed form."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _launch(2 if mode == "leaf_first" else 3 if _ngpu() >= 3 else 2, mode, 12, 29560 + len(mode))
