@@ -114,6 +114,9 @@ struct Ctx {
   DBuf<unsigned char> cub_tmp;
   DBuf<int> pcell_a, pcell_b, flags, scan, dflag;
   DBuf<int> leaf_ids;
+  DBuf<int> leaf_cls;                        // leaf ids by size class (P2P variants), counts below
+  int64_t leaf_cls_n[3] = {0, 0, 0};
+  bool leaf_cls_valid = false;
   Cells cells;
   int64_t ncells = 0, nleaves = 0;
   std::vector<int64_t> level_begin;          // cells of level l: [level_begin[l], level_begin[l+1])

@@ -66,6 +66,9 @@ namespace fmmb {
 
 namespace {
 
+#ifndef TC_OGROUP
+#define TC_OGROUP 0   // offsets per CTA (0: all of the level's); > 0 splits a row block's offsets over CTAs
+#endif
 #ifndef TC_CHUNK
 #define TC_CHUNK 32
 #endif
@@ -568,6 +571,7 @@ struct TcLevelArg {
   const unsigned* mask;          // per target cell (cell - lb) x W words: canonical offsets present
   const unsigned char* skip;     // per cell: 1 = every canonical offset, 2 = subset (mask)
   int ntgt, lt, D, cta_begin, lb, W;
+  int nblk, gsize;               // CTAs per offset group (row blocks), offsets per group
 };
 struct TcArgs {
   TcLevelArg lv[kMaxTcLevels];
@@ -583,7 +587,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   int li = 0;
   while (li + 1 < args.nlv && (int)blockIdx.x >= args.lv[li + 1].cta_begin) ++li;
   const TcLevelArg A = args.lv[li];
-  const int nit = A.D * kSPO;                   // pipeline stages
+  // offset groups: CTA (group, row block); all row blocks of a group run before the
+  // next group's, so concurrently running CTAs read the sources of nearby offsets
+  const int local = (int)blockIdx.x - A.cta_begin;
+  const int grp = local / A.nblk, blk = local - grp * A.nblk;
+  const int dbase = grp * A.gsize;
+  const int nit = min(A.gsize, A.D - dbase) * kSPO;   // pipeline stages
   constexpr int CN = kChunk * kSPO;
   const int nchunk = (nit + CN - 1) / CN;
 
@@ -605,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tbase;
-  const int row0 = ((int)blockIdx.x - A.cta_begin) * kRows;
+  const int row0 = blk * kRows;
 
   if (warp < kRows / 32) {
     // ---------------------------------------------------------- producers
@@ -632,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
     }
     int pf_d = -1;
     auto load = [&](int it, float (&v)[8 * kKPS]) {
-      const int d = it / kSPO, kb = (it - kSPO * (it / kSPO)) * kKPS;
+      const int d = dbase + it / kSPO, kb = (it - kSPO * (it / kSPO)) * kKPS;
       if (d != pf_d) {
         pf_d = d;
         on = allon || ((__ldg(mrow + (d >> 5)) >> (d & 31)) & 1u);
@@ -734,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (tid == 0) {
-            const int d = it / kSPO, kb = kb0;
+            const int d = dbase + it / kSPO, kb = kb0;
             const uint32_t bytes = (uint32_t)(T.opk[kb + kKPS] - T.opk[kb]);
             mbar_arrive_tx(&full[s], bytes);
             bulk_g2s(st + kAStage, A.op + (size_t)d * T.opk[kNKB] + T.opk[kb], bytes, &full[s]);
@@ -1047,9 +1056,11 @@ void m2l_tc_run(Ctx& c) {
     args.nlv = (int)std::min<size_t>(kMaxTcLevels, c.tc_levels.size() - g0);
     for (int i = 0; i < args.nlv; ++i) {
       const TcLevel& tl = c.tc_levels[g0 + i];
+      const int nblk = (int)((3 * (int64_t)tl.ntgt + kRows - 1) / kRows);
+      const int gsize = TC_OGROUP > 0 ? TC_OGROUP : tl.D;
       args.lv[i] = {c.tc_tgt2.p + tl.tgt_off, c.tc_codes.p + tl.code_off, c.tc_op.p + tl.op_off,
-                    c.tc_mask.p + tl.mask_off, c.tc_skip.p, tl.ntgt, tl.lt, tl.D, ctas, tl.lb, tl.W};
-      ctas += (int)((3 * (int64_t)tl.ntgt + kRows - 1) / kRows);
+                    c.tc_mask.p + tl.mask_off, c.tc_skip.p, tl.ntgt, tl.lt, tl.D, ctas, tl.lb, tl.W, nblk, gsize};
+      ctas += nblk * ((tl.D + gsize - 1) / gsize);
     }
     FMM_LAUNCH(c, k_m2l_tc, (unsigned)ctas, kThreads, smem, args, T, g, (const float4*)c.tc_mp.p, c.Lc.p);
   }

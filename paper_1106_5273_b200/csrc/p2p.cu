@@ -242,7 +242,14 @@ __global__ void k_leaf_local(const int* __restrict__ leaf, const unsigned char* 
   }
 }
 
-template <int MINB, int UF, int UN, bool ACC>
+// SPL > 1 (small target leaves, <= 64/SPL particles): the warp's lanes form SPL
+// groups holding the same 64/SPL targets (two per lane as always), and group g
+// takes sources g, g + SPL, ... of every tile (the tile's far and near parts are
+// padded with zero-strength sources to multiples of SPL so every lane runs the
+// same loop trips); each lane keeps its FP64 accumulators, and the groups' sums
+// are added in a fixed order at the end.  Lanes are otherwise idle on leaves
+// with few particles (adaptive trees, SURVEY 8d stress variants).
+template <int MINB, int UF, int UN, bool ACC, int SPL>
 __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_ids, const int* __restrict__ seg_b,
                                             const int* __restrict__ seg_e, const uint64_t* __restrict__ lst,
                                             PCells c, double lo0, double lo1, double lo2, double L,
@@ -250,14 +257,17 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                             const float4* __restrict__ posl, const float4* __restrict__ alp,
                                             float* __restrict__ un, float* __restrict__ sn,
                                             unsigned long long* __restrict__ near_pairs) {
-  __shared__ float4 sx[TP];   // (x', y', z', -log2(e)/(2 sigma^2))
-  __shared__ float4 sa[TP];   // (alpha/(4 pi), 1/(sqrt2 sigma))
-  __shared__ float4 sw[TP];   // alpha/(4 pi) x (y - C), C = the source leaf centre
-  __shared__ float4 sc[TP];   // near-kernel constants of the source (see pair2)
+  constexpr int NG = NT / SPL;        // lanes per source group
+  constexpr int TPASS = 2 * NG;       // targets per pass
+  __shared__ float4 sx[TP + 8];   // (x', y', z', -log2(e)/(2 sigma^2))
+  __shared__ float4 sa[TP + 8];   // (alpha/(4 pi), 1/(sqrt2 sigma))
+  __shared__ float4 sw[TP + 8];   // alpha/(4 pi) x (y - C), C = the source leaf centre
+  __shared__ float4 sc[TP + 8];   // near-kernel constants of the source (see pair2)
   __shared__ double sD[kDQ][NT];
   __shared__ float2 sB[3][NT];   // the lane's target alpha pairs (reloaded as aligned register pairs)
   const float k4 = (float)(1.0 / (4.0 * kPi));
   const int lane = threadIdx.x;
+  const int grpl = lane / NG, pl = lane - NG * (lane / NG);   // source group, target pair
   const int leaf = leaf_ids[blockIdx.x];
   const int lev = c.level[leaf], tb = c.begin[leaf], tcnt = c.count[leaf];
   const double s = L / (double)(1 << lev);
@@ -267,8 +277,8 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
   if (ACC && eb >= ee) return;                    // second pass (remote sources): nothing to add
   const float hst = (float)(0.5 * s);
   unsigned long long nnear = 0;                   // pairs evaluated with the regularised kernel
-  for (int t0 = 0; t0 < tcnt; t0 += TP) {
-    const int i0 = t0 + lane, i1 = t0 + lane + NT;
+  for (int t0 = 0; t0 < tcnt; t0 += TPASS) {
+    const int i0 = t0 + pl, i1 = t0 + pl + NG;
     const bool v0 = i0 < tcnt, v1 = i1 < tcnt;
     // absent targets sit far away so they never trigger the close-pair branch
     float x00 = 1e4f, x01 = 1e4f, x02 = 1e4f, x10 = 1e4f, x11 = 1e4f, x12 = 1e4f;
@@ -362,18 +372,32 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         const unsigned n0 = __ballot_sync(0xffffffffu, vj[0] && !fj[0]), n1 = __ballot_sync(0xffffffffu, vj[1] && !fj[1]);
         const int nfar = __popc(f0) + __popc(f1);
         const int nj = nfar + __popc(n0) + __popc(n1);
+        // SPL > 1: far and near parts padded to multiples of SPL
+        const int nfarP = (nfar + SPL - 1) / SPL * SPL;
+        const int njP = nfarP + (nj - nfar + SPL - 1) / SPL * SPL;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (!vj[h]) continue;
           const int dst = fj[h] ? (h == 0 ? __popc(f0 & lt) : __popc(f0) + __popc(f1 & lt))
-                                : nfar + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
+                                : nfarP + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
           sx[dst] = qv[h];
           sa[dst] = av[h];
           sw[dst] = wv[h];
           sc[dst] = cv[h];
         }
+        if (SPL > 1) {
+          // zero-strength padding sources far from the targets (finite kernel values)
+          const int pf = nfarP - nfar, pn = njP - nfarP - (nj - nfar);
+          if (lane < pf + pn) {
+            const int dst = lane < pf ? nfar + lane : njP - pn + (lane - pf);
+            sx[dst] = make_float4(1e4f, 1e4f, 1e4f, -1.4426950408889634f);
+            sa[dst] = make_float4(0.f, 0.f, 0.f, 1.f);
+            sw[dst] = make_float4(0.f, 0.f, 0.f, 0.f);
+            sc[dst] = make_float4(0.5f, 1.1283791670955126f, -0.75225277806367504f, 1.f);
+          }
+        }
         __syncwarp();
-        nnear += (unsigned long long)(nj - nfar) * (unsigned long long)min(TP, tcnt - t0);
+        nnear += (unsigned long long)(nj - nfar) * (unsigned long long)min(TPASS, tcnt - t0);
         {
           // reloaded per tile as 64-bit pairs so they sit in aligned register
           // pairs (otherwise ptxas re-pairs them with 6 MOVs per source: 218 -> 204 ms at C3)
@@ -388,37 +412,32 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         // amplifies their rounding by |x_i - C|/|r|; FP32 emulation at C4:
         // stretching rel-L2 8.9e-6 -> 4.6e-6).  P2P_ADJ_MODE 1 stages
         // such a leaf in tiles of 32 (emulation: 6.2e-6; 16: 4.6e-6 at +2 ms more); mode 0 chunks the loops; mode 2 does neither.
-#if P2P_ADJ_MODE == 0
-        const int cs = adj ? kAdjChunk : TP;
-        for (int c0 = 0; c0 < nj; c0 += cs) {
-          const int c1 = min(nj, c0 + cs), fe = min(c1, nfar);
-          Acc2 A;
-          zero(A);
-#pragma unroll UF
-          for (int jj = c0; jj < fe; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
-#pragma unroll UN
-          for (int jj = max(c0, nfar); jj < c1; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
-          flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
-        }
-#else
         Acc2 A;
         zero(A);
 #pragma unroll UF
-        for (int jj = 0; jj < nfar; ++jj) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
+        for (int jj = grpl; jj < nfarP; jj += SPL) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
 #pragma unroll UN
-        for (int jj = nfar; jj < nj; ++jj) pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+        for (int jj = nfarP + grpl; jj < njP; jj += SPL)
+          pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
         flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
-#endif
       }
     }
-    // s += (sum_j f alpha_j) x alpha_i
+    // s += (sum_j f alpha_j) x alpha_i; SPL > 1: the groups' sums, in group order
+    if (SPL > 1) __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (!(h == 0 ? v0 : v1)) continue;
+      if (!(h == 0 ? v0 : v1) || grpl != 0) continue;
       const float4 ai = h == 0 ? a0 : a1;
-      const double* D = &sD[9 * h][lane];
-      const double u0 = D[0 * NT], u1 = D[1 * NT], u2 = D[2 * NT], s0 = D[3 * NT], s1 = D[4 * NT], s2 = D[5 * NT];
-      const double f0 = D[6 * NT], f1 = D[7 * NT], f2 = D[8 * NT];
+      double Dv[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        double acc = sD[9 * h + q][pl];
+#pragma unroll
+        for (int k = 1; k < SPL; ++k) acc += sD[9 * h + q][pl + k * NG];
+        Dv[q] = acc;
+      }
+      const double u0 = Dv[0], u1 = Dv[1], u2 = Dv[2], s0 = Dv[3], s1 = Dv[4], s2 = Dv[5];
+      const double f0 = Dv[6], f1 = Dv[7], f2 = Dv[8];
       const int64_t o = 3 * (int64_t)(tb + (h == 0 ? i0 : i1));
       const float r[6] = {(float)u0, (float)u1, (float)u2, (float)(s0 + (f1 * ai.z - f2 * ai.y)),
                           (float)(s1 + (f2 * ai.x - f0 * ai.z)), (float)(s2 + (f0 * ai.y - f1 * ai.x))};
@@ -430,6 +449,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         sn[o] = r[3]; sn[o + 1] = r[4]; sn[o + 2] = r[5];
       }
     }
+    if (SPL > 1) __syncwarp();                    // the next pass clears sD
   }
   if (lane == 0 && nnear) atomicAdd(near_pairs, nnear);
 }
@@ -499,6 +519,21 @@ __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch
   }
 }
 
+// leaf size classes for the P2P variants: 0 = > 32 particles (SPL 1), 1 = 17..32 (SPL 2), 2 = <= 16 (SPL 4)
+__device__ __forceinline__ int leaf_class(int n) { return n > 32 ? 0 : (n > 16 ? 1 : 2); }
+__global__ void k_leaf_class_count(const int* __restrict__ ids, int64_t n, const int* __restrict__ count,
+                                   int* __restrict__ cnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[leaf_class(count[ids[k]])], 1);
+}
+__global__ void k_leaf_class_scatter(const int* __restrict__ ids, int64_t n, const int* __restrict__ count,
+                                     int o1, int o2, int* __restrict__ cnt, int* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int id = ids[k], cl = leaf_class(count[id]);
+    out[(cl == 0 ? 0 : cl == 1 ? o1 : o2) + atomicAdd(&cnt[cl], 1)] = id;
+  }
+}
+
 }  // namespace
 
 void eval_pair_kernel(Ctx& c, const float* rho, int64_t n, int branch, float* g, float* rgp) {
@@ -525,14 +560,35 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near, int part) {
                multi ? c.cflag.p : nullptr, pc, c0, c1, c.lo[0], c.lo[1], c.lo[2], c.L, c.pos.p, c.posl.p, c.alp.p);
   const int* sb = part == 2 ? c.p2p_m.p : c.p2p_b.p;
   const int* se = part == 1 ? c.p2p_m.p : c.p2p_e.p;
-  if (part == 2)
-    FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, true>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
-               c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
-               c.dnear.p);
-  else
-    FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, false>), (unsigned)c.nleaves, NT, 0, c.leaf_ids.p, sb, se, c.p2p.p, pc,
-               c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, u_near, s_near,
-               c.dnear.p);
+  // leaves by size class (once per set_particles): small leaves take the source-split variants
+  if (!c.leaf_cls_valid) {
+    c.leaf_cls.reserve(std::max<int64_t>(c.nleaves, 1));
+    c.dflag.reserve(8);
+    FMM_CUDA(cudaMemsetAsync(c.dflag.p, 0, sizeof(int) * 3, c.stream));
+    const unsigned g = (unsigned)std::min<int64_t>((c.nleaves + 255) / 256, 148 * 8);
+    FMM_LAUNCH(c, k_leaf_class_count, g, 256, 0, c.leaf_ids.p, (int64_t)c.nleaves, c.cells.count.p, c.dflag.p);
+    int h[3];
+    FMM_CUDA(cudaMemcpyAsync(h, c.dflag.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    FMM_CUDA(cudaStreamSynchronize(c.stream));
+    for (int k = 0; k < 3; ++k) c.leaf_cls_n[k] = h[k];
+    FMM_CUDA(cudaMemsetAsync(c.dflag.p, 0, sizeof(int) * 3, c.stream));
+    FMM_LAUNCH(c, k_leaf_class_scatter, g, 256, 0, c.leaf_ids.p, (int64_t)c.nleaves, c.cells.count.p, h[0], h[0] + h[1],
+               c.dflag.p, c.leaf_cls.p);
+    c.leaf_cls_valid = true;
+  }
+  const int* ids[3] = {c.leaf_cls.p, c.leaf_cls.p + c.leaf_cls_n[0], c.leaf_cls.p + c.leaf_cls_n[0] + c.leaf_cls_n[1]};
+#define P2P_ARGS sb, se, c.p2p.p, pc, c.lo[0], c.lo[1], c.lo[2], c.L, c.per[0], c.per[1], c.per[2], c.posl.p, c.alp.p, \
+                 u_near, s_near, c.dnear.p
+  if (part == 2) {
+    if (c.leaf_cls_n[0]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, true, 1>), (unsigned)c.leaf_cls_n[0], NT, 0, ids[0], P2P_ARGS);
+    if (c.leaf_cls_n[1]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, true, 2>), (unsigned)c.leaf_cls_n[1], NT, 0, ids[1], P2P_ARGS);
+    if (c.leaf_cls_n[2]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, true, 4>), (unsigned)c.leaf_cls_n[2], NT, 0, ids[2], P2P_ARGS);
+  } else {
+    if (c.leaf_cls_n[0]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, false, 1>), (unsigned)c.leaf_cls_n[0], NT, 0, ids[0], P2P_ARGS);
+    if (c.leaf_cls_n[1]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, false, 2>), (unsigned)c.leaf_cls_n[1], NT, 0, ids[1], P2P_ARGS);
+    if (c.leaf_cls_n[2]) FMM_LAUNCH(c, (k_p2p<P2P_MINB, P2P_UF, P2P_UN, false, 4>), (unsigned)c.leaf_cls_n[2], NT, 0, ids[2], P2P_ARGS);
+  }
+#undef P2P_ARGS
 }
 
 void eval_cutoff(Ctx& c, const float* rho, int64_t n, float* g) {

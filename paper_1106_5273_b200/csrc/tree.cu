@@ -324,6 +324,7 @@ void set_particles_impl(Ctx& c, int64_t n, const float* x, const float* a, const
   c.ncells = c.nloc_cells = 0;
   c.nleaves = 0;
   c.nsrc = 0;
+  c.leaf_cls_valid = false;
   c.level_begin.assign(1, 0);
   FMM_CUDA(cudaEventRecord(c.ev[PH_SET0], st));
 
