@@ -97,6 +97,9 @@ struct Ctx {
   DBuf<float> ret_send, ret_recv, loc_u, loc_s;
   // tensor-core M2L source map for forests (m2l_tc.cu): level grid -> cell id
   DBuf<int> tc_map;
+  bool tc_use_map = false;
+  bool tc_mixed = false;                     // some taken cell keeps register-path entries (per-entry select)
+  DBuf<unsigned char> tc_extra;
   std::vector<int64_t> tc_map_off;
 
   // ---- particles and tree (set_particles) ----

@@ -402,7 +402,8 @@ __global__ void k_tc_count_has(const unsigned char* __restrict__ has, TcVer v, i
 // register kernel, whichever path takes the target's canonical ones.
 __global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
                                     const short* __restrict__ tbl, unsigned* __restrict__ mask,
-                                    unsigned char* __restrict__ bad, unsigned* __restrict__ goodw) {
+                                    unsigned char* __restrict__ bad, unsigned* __restrict__ goodw,
+                                    unsigned char* __restrict__ extra) {
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; i0 < n;
        i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + (threadIdx.x & 31);
@@ -434,6 +435,8 @@ __global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n,
           const unsigned bit = 1u << (d & 31);
           const unsigned old = atomicOr(&mask[v.mask_off[k] + row * v.W[k] + (d >> 5)], bit);
           if (old & bit) bad[v.lb[k] + row] = 1;
+        } else {
+          extra[t] = 1;                        // an entry the register kernel keeps
         }
       }
     }
@@ -449,7 +452,8 @@ __global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n,
 constexpr float kMinFrac = 0.4f;
 __global__ void k_tc_accept(TcVer v, const unsigned* __restrict__ mask, const unsigned char* __restrict__ bad,
                             unsigned char* __restrict__ skip, int* __restrict__ tgt, const int64_t* __restrict__ tgt_off,
-                            int* __restrict__ ntgt, unsigned long long* __restrict__ nent) {
+                            int* __restrict__ ntgt, unsigned long long* __restrict__ nent,
+                            const unsigned char* __restrict__ extra, int* __restrict__ mixed) {
   for (int k = 0; k < v.nlv; ++k) {
     for (int c = v.lb[k] + (int)(blockIdx.x * blockDim.x + threadIdx.x); c < v.le[k]; c += (int)(gridDim.x * blockDim.x)) {
       if (bad[c]) continue;
@@ -460,6 +464,7 @@ __global__ void k_tc_accept(TcVer v, const unsigned* __restrict__ mask, const un
         skip[c] = pc == v.D[k] ? 1 : 2;          // 1: every canonical offset (no mask lookups), 2: masked
         tgt[tgt_off[k] + atomicAdd(&ntgt[k], 1)] = c;
         atomicAdd(nent, (unsigned long long)pc);
+        if (pc != v.D[k] || extra[c]) *mixed = 1;   // the register kernel keeps entries of a taken cell
       }
     }
   }
@@ -823,7 +828,7 @@ TcGeo make_geo(Ctx& c) {
   for (int a = 0; a < 3; ++a) g.per[a] = c.per_units[a];
   const int nl = (int)c.level_begin.size();
   for (int l = 0; l < kMaxLevel + 2; ++l) g.lvl_begin[l] = (int)c.level_begin[std::min(l, nl - 1)];
-  g.map = c.cfg.nranks > 1 ? c.tc_map.p : nullptr;
+  g.map = c.tc_use_map ? c.tc_map.p : nullptr;
   for (int l = 0; l < kMaxLevel + 2; ++l) g.map_off[l] = l < (int)c.tc_map_off.size() ? (int)c.tc_map_off[l] : -1;
   return g;
 }
@@ -843,6 +848,7 @@ void tc_cub(Ctx& c, F f) {
 // build) and build their operators.  Host-synchronous (small copies).
 void m2l_tc_prepare(Ctx& c) {
   c.tc_valid = true;
+  c.tc_mixed = false;
   c.tc_levels.clear();
   c.tc_entries = 0;
   c.tc_skip.reserve(std::max<int64_t>(c.ncells, 1));
@@ -856,10 +862,25 @@ void m2l_tc_prepare(Ctx& c) {
   FMM_LAUNCH(c, k_tc_cq, (unsigned)std::min<int64_t>((c.ncells + 255) / 256, 148 * 8), 256, 0, c.cells.qx.p,
              c.cells.qy.p, c.cells.qz.p, c.cells.level.p, (int64_t)c.ncells, c.tc_cq.p);
   // candidate target levels: >= 1024 cells (smaller levels: the register kernel is as fast)
-  auto candidate = [&](int l) {
-    return l >= 2 && l < nlev && c.level_begin[l + 1] - c.level_begin[l] >= 1024 && (c.cfg.nranks == 1 || l + 1 <= kMaxMapLevel);
+  // one GPU: a level is "full" when it holds every cell of its grid inside the
+  // periodic domain, and tc_source is then the Morton index within the level;
+  // otherwise (adaptive trees: partial levels) and on several GPUs (forests)
+  // sources are found through per-level maps
+  const int64_t tprod = (int64_t)c.cfg.tiles[0] * c.cfg.tiles[1] * c.cfg.tiles[2];
+  auto full_level = [&](int l) {
+    if (l < 0 || l >= nlev) return false;
+    const int64_t want = (1ll << (3 * l)) * tprod / ((int64_t)c.tmax * c.tmax * c.tmax);
+    return c.level_begin[l + 1] - c.level_begin[l] == want;
   };
-  if (c.cfg.nranks > 1) {
+  auto big = [&](int l) { return l >= 2 && l < nlev && c.level_begin[l + 1] - c.level_begin[l] >= 1024; };
+  bool any_partial = false;
+  for (int l = 2; l < nlev; ++l)
+    if (big(l))
+      for (int ls = l - 1; ls <= l + 1; ++ls)
+        if (ls < nlev && !full_level(ls) && !(ls == l + 1 && ls == nlev)) any_partial = true;
+  c.tc_use_map = c.cfg.nranks > 1 || any_partial;
+  auto candidate = [&](int l) { return big(l) && (!c.tc_use_map || l + 1 <= kMaxMapLevel); };
+  if (c.tc_use_map) {
     // LET forest: sources are found through a per-level map of all trees' cells,
     // built for the source levels (lt - 1, lt, lt + 1) of every candidate level;
     // a level without a map makes tc_source return -1 (entry fails -> register kernel)
@@ -976,16 +997,23 @@ void m2l_tc_prepare(Ctx& c) {
   FMM_CUDA(cudaMemsetAsync(c.tc_good.p, 0, sizeof(unsigned) * ((c.nm2l + 31) / 32 + 1), st));
   c.dcount.reserve(1);
   FMM_CUDA(cudaMemsetAsync(c.dcount.p, 0, sizeof(unsigned long long), st));
+  c.tc_tmp.reserve(kMaxLevel + 2);
+  c.tc_extra.reserve(std::max<int64_t>(c.ncells, 1));
+  FMM_CUDA(cudaMemsetAsync(c.tc_extra.p, 0, std::max<int64_t>(c.ncells, 1), st));
+  FMM_CUDA(cudaMemsetAsync(c.tc_tmp.p, 0, sizeof(int), st));
   FMM_LAUNCH(c, k_tc_verify_entries, gl, 256, 0, c.m2l.p, c.nm2l, w, g, c.tc_tbl.p, c.tc_mask.p, c.tc_bad.p,
-             c.tc_good.p);
+             c.tc_good.p, c.tc_extra.p);
   FMM_LAUNCH(c, k_tc_accept, 148 * 4, 256, 0, w, c.tc_mask.p, c.tc_bad.p, c.tc_skip.p, c.tc_tgt.p, c.tc_off.p,
-             c.tc_cnt.p, c.dcount.p);
+             c.tc_cnt.p, c.dcount.p, c.tc_extra.p, c.tc_tmp.p);
   FMM_CUDA(cudaStreamSynchronize(st));    // host vectors above are read by the copies
   std::vector<int> cnt(cands.size());
   unsigned long long nent = 0;
+  int mixed = 0;
   FMM_CUDA(cudaMemcpyAsync(cnt.data(), c.tc_cnt.p, sizeof(int) * cands.size(), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaMemcpyAsync(&nent, c.dcount.p, sizeof(nent), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(&mixed, c.tc_tmp.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
+  c.tc_mixed = mixed != 0;                 // else a taken cell's entries are all on the tensor path
   // Morton order of the targets (= cell index order within a level)
   for (size_t i = 0; i < cands.size(); ++i) {
     const int n = cnt[i];

@@ -177,6 +177,11 @@ void sort_list(Ctx& c, DBuf<uint64_t>& lst, int64_t n, int begin_bit = 0) {
 
 }  // namespace
 
+struct NotTaken {
+  const unsigned char* skip;
+  __device__ __forceinline__ bool operator()(const uint64_t& e) const { return !skip[(int)(e >> 32)]; }
+};
+
 // entry i stays on the register kernel unless its target is on the tensor path
 // and the tensor path verified this entry (m2l_tc_prepare's per-entry bits)
 struct OnRegisterPath {
@@ -204,12 +209,20 @@ void m2l_reg_segments(Ctx& c) {
   uint64_t* out = c.m2lr.p;
   int* nsel = c.dsel.p;
   const int n = (int)c.nm2l;
-  cub::CountingInputIterator<int64_t> idx(0);
-  cub::TransformInputIterator<char, OnRegisterPath, cub::CountingInputIterator<int64_t>> flags(
-      idx, OnRegisterPath{c.m2l.p, c.tc_skip.p, c.tc_good.p});
-  cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, nsel, n, st);
-  });
+  if (c.tc_mixed) {
+    cub::CountingInputIterator<int64_t> idx(0);
+    cub::TransformInputIterator<char, OnRegisterPath, cub::CountingInputIterator<int64_t>> flags(
+        idx, OnRegisterPath{c.m2l.p, c.tc_skip.p, c.tc_good.p});
+    cub_call(c, [&](void* tmp, size_t& bytes) {
+      return cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, nsel, n, st);
+    });
+  } else {
+    // every entry of a taken cell is on the tensor path (uniform levels): by target alone
+    NotTaken pred{c.tc_skip.p};
+    cub_call(c, [&](void* tmp, size_t& bytes) {
+      return cub::DeviceSelect::If(tmp, bytes, in, out, nsel, n, pred, st);
+    });
+  }
   int ns = 0;
   FMM_CUDA(cudaMemcpyAsync(&ns, c.dsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
@@ -306,13 +319,17 @@ void build_lists(Ctx& c) {
     nf = add_q;
   }
 
-  // per-target segments: P2P in canonical order (it fixes the near-field
-  // summation order, identical on 1 and N GPUs).  The M2L list stays in the
+  // per-target segments of the P2P list (fixes the near-field summation
+  // order; deterministic).  The M2L list stays in the
   // traversal's (deterministic) emission order: the tensor path verifies it
   // entry by entry, and only the entries it does not take are grouped by
   // target for the register kernels (m2l_reg_segments, after m2l_tc_prepare);
   // fmm_get_lists returns the canonical order
-  sort_list(c, c.p2p, c.np2p);
+  // one GPU: grouped by target only (stable radix sort on the target bits, 3
+  // passes instead of 7: the sources of a target keep the traversal's
+  // deterministic emission order); several GPUs: canonical, so that the local
+  // sources (ids < nloc) precede the received ones in every target's segment
+  sort_list(c, c.p2p, c.np2p, multi ? 0 : 32);
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
   FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
   if (c.np2p) FMM_LAUNCH(c, k_segments, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
