@@ -358,16 +358,19 @@ __device__ __forceinline__ int ver_level(const TcVer& v, int t) {
 constexpr int kHR = 24;                 // |v| <= 24 finest-level units: covers the theta = 1/2 lists
 constexpr int kHV = 2 * kHR + 1;
 constexpr int kHBins = 3 * kHV * kHV * kHV;
-constexpr int kHSample = 16;             // the histogram samples every 16th cell (163M atomics on ~550 bins otherwise)
+constexpr int kHSample = 16;             // the histogram samples 1/16 of the entries (163M atomics on ~550 bins otherwise)
 __global__ void k_tc_code_hist(const uint64_t* __restrict__ lst, int64_t n, TcVer v, TcGeo g,
                                unsigned* __restrict__ hist) {
+  // a sample of the list: runs of 16 consecutive entries (one 128-byte line), each run taken
+  // with probability 1/16 by a multiplicative hash of its index (no aliasing with the
+  // traversal's regular emission pattern)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if ((((uint32_t)(i >> 4) * 2654435761u) >> 28) != 0) continue;
     const uint64_t ent = lst[i];
     const int t = (int)(ent >> 32);
     const int k = ver_level(v, t);
     if (k < 0) continue;
     const int lt = v.lt[k];
-    if ((t - v.lb[k]) & (kHSample - 1)) continue;     // every kHSample-th cell of the level
     const int4 tq = __ldg(g.cq + t);
     long long ct[3];
     ct[0] = (long long)(2 * tq.x + 1) << (kMaxLevel - lt);
@@ -386,7 +389,7 @@ __global__ void k_tc_count_has(const unsigned char* __restrict__ has, TcVer v, i
   for (int k = 0; k < v.nlv; ++k) {
     int m = 0;
     for (int c = v.lb[k] + (int)(blockIdx.x * blockDim.x + threadIdx.x); c < v.le[k]; c += (int)(gridDim.x * blockDim.x))
-      m += (has[c] && !((c - v.lb[k]) & (kHSample - 1))) ? 1 : 0;
+      m += has[c] ? 1 : 0;
     for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(&cnt[k], m);
   }
@@ -938,7 +941,7 @@ void m2l_tc_prepare(Ctx& c) {
         for (int y = -kHR; y <= kHR; ++y)
           for (int z = -kHR; z <= kHR; ++z) {
             const unsigned h = hist[(size_t)k * kHBins + (((dl + 1) * kHV + x + kHR) * kHV + y + kHR) * kHV + z + kHR];
-            if (2ll * h > (long long)nhas[k]) cd.codes.push_back(((dl + 1) << 21) | ((x + 64) << 14) | ((y + 64) << 7) | (z + 64));
+            if (2ll * kHSample * h > (long long)nhas[k]) cd.codes.push_back(((dl + 1) << 21) | ((x + 64) << 14) | ((y + 64) << 7) | (z + 64));
           }
     cd.D = (int)cd.codes.size();
     if (cd.D == 0) continue;

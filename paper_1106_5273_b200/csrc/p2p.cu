@@ -31,6 +31,8 @@
 // there 1 - g < 4e-9 and rho g' = (4/sqrt pi) rho^3 e^{-rho^2} < 1.5e-7 (both
 // within reading Z6's 2e-7), so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
 // fmm_eval_pair_kernel exports both branches' g and rho g' for the Z6 test.
+#include <cub/cub.cuh>
+
 #include "ctx.cuh"
 
 namespace fmmb {
@@ -521,18 +523,11 @@ __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch
 
 // leaf size classes for the P2P variants: 0 = > 32 particles (SPL 1), 1 = 17..32 (SPL 2), 2 = <= 16 (SPL 4)
 __device__ __forceinline__ int leaf_class(int n) { return n > 32 ? 0 : (n > 16 ? 1 : 2); }
-__global__ void k_leaf_class_count(const int* __restrict__ ids, int64_t n, const int* __restrict__ count,
-                                   int* __restrict__ cnt) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&cnt[leaf_class(count[ids[k]])], 1);
-}
-__global__ void k_leaf_class_scatter(const int* __restrict__ ids, int64_t n, const int* __restrict__ count,
-                                     int o1, int o2, int* __restrict__ cnt, int* __restrict__ out) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int id = ids[k], cl = leaf_class(count[id]);
-    out[(cl == 0 ? 0 : cl == 1 ? o1 : o2) + atomicAdd(&cnt[cl], 1)] = id;
-  }
-}
+struct LeafClass {
+  const int* count;
+  int cl;
+  __device__ __forceinline__ bool operator()(const int& id) const { return leaf_class(count[id]) == cl; }
+};
 
 }  // namespace
 
@@ -562,18 +557,28 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near, int part) {
   const int* se = part == 1 ? c.p2p_m.p : c.p2p_e.p;
   // leaves by size class (once per set_particles): small leaves take the source-split variants
   if (!c.leaf_cls_valid) {
+    // stable (Morton order kept within a class: neighbouring blocks then share their
+    // source leaves in L2; an atomic scatter scrambled it: +0.9 ms at C3)
     c.leaf_cls.reserve(std::max<int64_t>(c.nleaves, 1));
     c.dflag.reserve(8);
-    FMM_CUDA(cudaMemsetAsync(c.dflag.p, 0, sizeof(int) * 3, c.stream));
-    const unsigned g = (unsigned)std::min<int64_t>((c.nleaves + 255) / 256, 148 * 8);
-    FMM_LAUNCH(c, k_leaf_class_count, g, 256, 0, c.leaf_ids.p, (int64_t)c.nleaves, c.cells.count.p, c.dflag.p);
-    int h[3];
-    FMM_CUDA(cudaMemcpyAsync(h, c.dflag.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    FMM_CUDA(cudaStreamSynchronize(c.stream));
-    for (int k = 0; k < 3; ++k) c.leaf_cls_n[k] = h[k];
-    FMM_CUDA(cudaMemsetAsync(c.dflag.p, 0, sizeof(int) * 3, c.stream));
-    FMM_LAUNCH(c, k_leaf_class_scatter, g, 256, 0, c.leaf_ids.p, (int64_t)c.nleaves, c.cells.count.p, h[0], h[0] + h[1],
-               c.dflag.p, c.leaf_cls.p);
+    int off = 0;
+    for (int cl = 0; cl < 3; ++cl) {
+      LeafClass pred{c.cells.count.p, cl};
+      const int* in = c.leaf_ids.p;
+      int* out = c.leaf_cls.p + off;
+      int* ns = c.dflag.p;
+      const int nn = (int)c.nleaves;
+      size_t bytes = 0;
+      FMM_CUDA(cub::DeviceSelect::If(nullptr, bytes, in, out, ns, nn, pred, c.stream));
+      c.cub_tmp.reserve(bytes);
+      FMM_CUDA(cub::DeviceSelect::If((void*)c.cub_tmp.p, bytes, in, out, ns, nn, pred, c.stream));
+      ++c.cub_calls;
+      int h = 0;
+      FMM_CUDA(cudaMemcpyAsync(&h, c.dflag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      FMM_CUDA(cudaStreamSynchronize(c.stream));
+      c.leaf_cls_n[cl] = h;
+      off += h;
+    }
     c.leaf_cls_valid = true;
   }
   const int* ids[3] = {c.leaf_cls.p, c.leaf_cls.p + c.leaf_cls_n[0], c.leaf_cls.p + c.leaf_cls_n[0] + c.leaf_cls_n[1]};

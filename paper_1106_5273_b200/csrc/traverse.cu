@@ -325,11 +325,13 @@ void build_lists(Ctx& c) {
   // entry by entry, and only the entries it does not take are grouped by
   // target for the register kernels (m2l_reg_segments, after m2l_tc_prepare);
   // fmm_get_lists returns the canonical order
-  // one GPU: grouped by target only (stable radix sort on the target bits, 3
-  // passes instead of 7: the sources of a target keep the traversal's
-  // deterministic emission order); several GPUs: canonical, so that the local
-  // sources (ids < nloc) precede the received ones in every target's segment
-  sort_list(c, c.p2p, c.np2p, multi ? 0 : 32);
+  // canonical (target, source, image) order: consecutive target leaves then
+  // read their source leaves in nearly the same order, which keeps the P2P
+  // kernel's source reads in L2 (grouped by target only, the traversal's
+  // emission order saves 1.8 ms of sorting but raises the P2P kernel's DRAM
+  // traffic from 1.8 to 10.2 GB per launch, r02 prof2), and on several GPUs the
+  // local sources (ids < nloc) precede the received ones in every segment
+  sort_list(c, c.p2p, c.np2p);
   c.p2p_b.reserve(c.ncells); c.p2p_e.reserve(c.ncells);
   FMM_LAUNCH(c, k_clear2, nblocks(c.ncells, 256), 256, 0, c.p2p_b.p, c.p2p_e.p, c.ncells);
   if (c.np2p) FMM_LAUNCH(c, k_segments, nblocks(c.np2p, 256), 256, 0, c.p2p.p, c.np2p, c.p2p_b.p, c.p2p_e.p);
