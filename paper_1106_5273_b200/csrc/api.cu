@@ -152,10 +152,22 @@ void evaluate_impl(Ctx& c, int parts, float* u, float* s) {
   const int conc = multi ? 0 : c.concurrent;
   if (conc == 0) {
     FMM_CUDA(cudaEventRecord(c.ev[PH_P2P], st));     // (multi: start of the part after the LET)
-    // a9 M2L + a8 periodic far layers
+    // a8 periodic far layers (beside the M2L on the side stream: they read only the
+    // top multipoles and write their own partials) + a9 M2L, then the far reduction
     FMM_CUDA(cudaMemsetAsync(c.Lc.p, 0, ncoef * sizeof(float2), st));
+    FMM_CUDA(cudaStreamWaitEvent(c.mstream, c.ev[PH_P2P], 0));
+    std::swap(c.stream, c.mstream);
+    try {
+      periodic_far_pass(c, 1);
+      FMM_CUDA(cudaEventRecord(c.ev_far, c.stream));
+    } catch (...) {
+      std::swap(c.stream, c.mstream);
+      throw;
+    }
+    std::swap(c.stream, c.mstream);
     m2l_pass(c);
-    periodic_far_pass(c);
+    FMM_CUDA(cudaStreamWaitEvent(st, c.ev_far, 0));
+    periodic_far_pass(c, 2);
     FMM_CUDA(cudaEventRecord(c.ev[PH_M2L], st));
     // a12 (multi: the received sources' entries, added)
     p2p_pass(c, c.u_near.p, c.s_near.p, multi ? 2 : 0);
@@ -309,6 +321,7 @@ FMM_API fmm_status fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     FMM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     FMM_CUDA(cudaEventCreate(&c.ev_trav));
     for (auto& e : c.ev_m2l) FMM_CUDA(cudaEventCreate(&e));
+    FMM_CUDA(cudaEventCreateWithFlags(&c.ev_far, cudaEventDisableTiming));
     set_expansion_smem_limits();
     FMM_CUDA(cudaGetLastError());
     comm_init(c);
@@ -332,6 +345,7 @@ FMM_API fmm_status fmm_destroy(fmm_ctx* h) {
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_trav) cudaEventDestroy(c.ev_trav);
   for (auto e : c.ev_m2l) if (e) cudaEventDestroy(e);
+  if (c.ev_far) cudaEventDestroy(c.ev_far);
   if (c.stream2) cudaStreamDestroy(c.stream2);
   try { comm_destroy(c); } catch (...) {}
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);

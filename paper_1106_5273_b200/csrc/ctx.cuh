@@ -158,6 +158,8 @@ struct Ctx {
   int r8_order = 0;
   DBuf<double> far_M;                        // periodic super-cell multipoles
   DBuf<double2> far_part;                    // per-chunk partial far-field locals
+  DBuf<int> far_tg;                          // far-field target cells
+  int far_ntg = 0, far_nchunk = 0;
   DBuf<float> u_near, s_near, u_far, s_far;  // sorted order, [n][3]
   DBuf<float> stage_u, stage_ds;             // host-output staging
   bool evaluated = false;
@@ -177,6 +179,7 @@ struct Ctx {
   cudaEvent_t ev[PH_N + 1] = {};
   cudaEvent_t ev_fork = nullptr, ev_trav = nullptr;   // upward-pass / traversal overlap
   cudaEvent_t ev_m2l[3] = {};                          // M2L sub-phases: start, tensor done, register done
+  cudaEvent_t ev_far = nullptr;                        // far layers (phase 1) done on the side stream
   bool overlapped = false;
   fmm_stats stats{};
 };
@@ -213,7 +216,7 @@ void orb_redistribute(Ctx& c, int64_t n, const float* x, const float* a, const f
 void orb_return(Ctx& c, const float* u_loc, const float* s_loc, float* u, float* s);
 void step_stage_update(Ctx& c, const float* x, const float* a, const float* s, const float* u, const float* da,
                        int64_t n, double h, double two_nu_t, float* xo, float* ao, float* so);
-void periodic_far_pass(Ctx& c);
+void periodic_far_pass(Ctx& c, int phase = 3);
 void fill_f32(Ctx& c, float* p, int64_t n, float v);
 void downward_pass(Ctx& c, float* u_far, float* s_far);
 void p2p_pass(Ctx& c, float* u_near, float* s_near, int part = 0);   // part: 0 all, 1 local sources, 2 remote (adds)

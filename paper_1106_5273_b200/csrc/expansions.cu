@@ -547,10 +547,20 @@ void m2l_pass(Ctx& c) {
   FMM_CUDA(cudaEventRecord(c.ev_m2l[2], c.stream));
 }
 
-void periodic_far_pass(Ctx& c) {
+// phase 1: the super-cell multipoles and the far layers' M2L into per-chunk
+// partials (independent of the M2L list: may run beside it); phase 2: the
+// fixed-order reduction of the partials into the locals; 3: both
+void periodic_far_pass(Ctx& c, int phase) {
   int k = c.cfg.images;
+  if (phase & 1) c.far_ntg = 0;
+  if (k < 2 || c.ncells == 0) { if (phase & 1) c.far_m2l = 0; return; }
+  if (!(phase & 1)) {
+    if (c.far_ntg > 0)
+      FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)c.far_ntg * 3 * c.nc, 128), 128, 0, c.nc, c.far_nchunk, c.far_tg.p,
+                 c.far_ntg, c.far_part.p, c.Lc.p);
+    return;
+  }
   c.far_m2l = 0;
-  if (k < 2 || c.ncells == 0) return;
   int P = c.P, nc = c.nc, P2 = P, nc2 = P2 * (P2 + 1) / 2;
   // far targets: cells of side box_len / 4 (level 2 + log2 tmax) and leaves above
   // (this rank's cells only)
@@ -571,16 +581,20 @@ void periodic_far_pass(Ctx& c) {
   c.far_M.reserve((size_t)k * 3 * nc * 2);
   FMM_LAUNCH(c, k_far_super, 1, round32(3 * nc), sizeof(double) * 2 * nc, P, k, geo(c), c.top_M.p, c.far_M.p);
   FMM_LAUNCH_CHECK();
-  c.scan.reserve(tg.size() + 1);   // reuse as a small int buffer
-  FMM_CUDA(cudaMemcpyAsync(c.scan.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
+  c.far_tg.reserve(tg.size() + 1);
+  // (pageable source: the call returns once tg has been staged, so tg may go)
+  FMM_CUDA(cudaMemcpyAsync(c.far_tg.p, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice, c.stream));
   size_t sm = sizeof(double) * 2 * (nc2 + 3 * nc);
   const int ntg = (int)tg.size(), nchunk = 26 * (k - 1);
   c.far_part.reserve((size_t)nchunk * ntg * 3 * nc);
   const int ntile = c.tmax > 1 ? c.cfg.tiles[0] * c.cfg.tiles[1] * c.cfg.tiles[2] : 0;
-  FMM_LAUNCH(c, k_far_m2l, dim3(ntg, nchunk), round32(nc), sm, P, k, c.scan.p, ntg, gcells(c), geo(c), c.far_M.p,
+  FMM_LAUNCH(c, k_far_m2l, dim3(ntg, nchunk), round32(nc), sm, P, k, c.far_tg.p, ntg, gcells(c), geo(c), c.far_M.p,
              ntile, c.top_M.p, c.far_part.p);
-  FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)ntg * 3 * nc, 128), 128, 0, nc, nchunk, c.scan.p, ntg, c.far_part.p,
-             c.Lc.p);
+  c.far_ntg = ntg;
+  c.far_nchunk = nchunk;
+  if (phase & 2)
+    FMM_LAUNCH(c, k_far_reduce, nblocks((int64_t)ntg * 3 * nc, 128), 128, 0, nc, nchunk, c.far_tg.p, ntg, c.far_part.p,
+               c.Lc.p);
   FMM_LAUNCH_CHECK();
   c.far_m2l = (int64_t)tg.size() * 702 * (k - 1 + (ntile > 1 ? ntile - 1 : 0));
 }
