@@ -152,8 +152,10 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
   const float2 rx = __fadd2_rn(x0, bc(-q.x)), ry = __fadd2_rn(x1, bc(-q.y)), rz = __fadd2_rn(x2, bc(-q.z));
   const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
   float2 inv;
-  if (NEAR) inv = make_float2(rsqrt_approx(fmaxf(r2.x, 1e-12f)), rsqrt_approx(fmaxf(r2.y, 1e-12f)));
-  else inv = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));      // rho >= 4.6: r > 0
+  // r = 0 (the self pair) gives inf/NaN here, but such a pair always takes the
+  // close-pair series below (its rho^2 = 0 votes the warp in), which replaces f
+  // and f'/r by selection; rho >= 4.6 in the singular branch: r > 0
+  inv = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
   const float2 inv2 = __fmul2_rn(inv, inv);
   const float2 inv3 = __fmul2_rn(inv2, inv);
   float2 f, fp3;
