@@ -340,6 +340,13 @@ def main():
     phase = {k: statistics.median(st[k] for st in stats) for k in
              ("ms_keys", "ms_sort", "ms_tree", "ms_upward", "ms_traverse", "ms_m2l", "ms_m2l_tc", "ms_m2l_reg",
               "ms_p2p", "ms_downward", "ms_finalize", "ms_set_total", "ms_eval_total")}
+    phase_ranks = [phase]
+    if world > 1:
+        phase_ranks = [None] * world
+        mine = {k: round(v, 3) for k, v in phase.items()}
+        mine.update({k: stats[-1][k] for k in ("n", "nleaves", "ncells_local", "ncells", "p2p_list", "p2p_pairs",
+                                               "p2p_near_pairs", "m2l_list", "m2l_reg_list")})
+        dist.all_gather_object(phase_ranks, mine)
     m2l_split = {k: stats[-1][k] for k in ("m2l_list", "m2l_tc_list", "m2l_reg_list")}
     m2l_split["tc_fraction"] = m2l_split["m2l_tc_list"] / max(1, m2l_split["m2l_list"])
     m2l_split["reg_kernel_tflops_algorithmic"] = (29040.0 * m2l_split["m2l_reg_list"] / (phase["ms_m2l_reg"] * 1e-3) / 1e12
@@ -462,6 +469,7 @@ def main():
             "p2p_pairs_per_step": int(tot_pairs), "model_flops_per_step": FLOPS_PER_PAIR * tot_pairs,
             "particles_per_s": tot_n / (ms_max * 1e-3),
             "phases_ms": phase,
+            "phases_ms_per_rank": phase_ranks if world > 1 else None,
             "m2l_split": m2l_split,
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -16,8 +16,12 @@
 // is exact): eight passes of 8 bits, each a per-rank device histogram of
 // every active group's candidates followed by one NCCL all-reduce of the
 // histograms -- no sort anywhere, as the paper's nth-element is "much faster
-// than any sorting algorithm".  The subdomains are the (rectangular) ORB boxes
-// the dual traversal and the LET handle.
+// than any sorting algorithm".  One more counting pass (k_orb_tie) moves a
+// cut that would leave a sparse sliver of a lattice plane on one side to the
+// plane's edge (reading Z28): such slivers, on the far side of an octant
+// boundary, became coarse leaves with near lists of ~10^5 leaves.  The
+// subdomains are the (rectangular) ORB boxes the dual traversal and the LET
+// handle.
 //
 // Redistribution: every particle goes to the rank of its final group
 // (records grouped by owner with a stable 4-bit radix sort, grouped
@@ -62,6 +66,24 @@ __global__ void k_orb_hist(const float4* __restrict__ pos, int64_t n, const unsi
   __syncthreads();
   for (int i = threadIdx.x; i < op.ngroups * 256; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+// per active group: particles whose axis coordinate lies below / on the
+// selected element's coordinate (cnt[2 g] / cnt[2 g + 1])
+__global__ void k_orb_tie(const float4* __restrict__ pos, int64_t n, const unsigned char* __restrict__ grp,
+                          OrbPass op, unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned int sh[2 * kMaxGroups];
+  if (threadIdx.x < 2 * kMaxGroups) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = grp[i];
+    if (!op.active[g]) continue;
+    const uint32_t cb = (uint32_t)(orb_key(pos[i], op.axis[g], 0u) >> 32), cs = (uint32_t)(op.prefix[g] >> 32);
+    if (cb < cs) atomicAdd(&sh[2 * g], 1u);
+    else if (cb == cs) atomicAdd(&sh[2 * g + 1], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * kMaxGroups && sh[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], (unsigned long long)sh[threadIdx.x]);
 }
 
 // split: particles of an active group with key < prefix (the selected
@@ -207,13 +229,33 @@ static void orb_groups(Ctx& c, const float4* pos, int64_t n, bool reuse, std::ve
           op.prefix[gi] |= (unsigned long long)dg << op.shift;
         }
       }
+      // ties (reading Z28): when the selected element's coordinate is shared by
+      // a plane of particles and only a sparse part of that plane (< 1/4) would
+      // fall on one side, the cut moves to the plane's boundary (cost <= 5% of
+      // a rank's share); otherwise the id tie-break keeps the split exact
+      FMM_CUDA(cudaMemsetAsync(c.orb_hist.p, 0, sizeof(unsigned long long) * 2 * kMaxGroups, st));
+      if (n > 0) FMM_LAUNCH(c, k_orb_tie, grid_for(n), 256, 0, pos, n, c.orb_grp.p, op, c.orb_hist.p);
+      allreduce_sum_u64(c, c.orb_hist.p, 2 * kMaxGroups);
+      FMM_CUDA(cudaMemcpyAsync(h.data(), c.orb_hist.p, sizeof(unsigned long long) * 2 * kMaxGroups,
+                               cudaMemcpyDeviceToHost, st));
+      FMM_CUDA(cudaStreamSynchronize(st));
       // relabel: active groups split into (low, high), the others keep one id
       std::vector<G> next;
       for (int gi = 0; gi < op.ngroups; ++gi) {
         const G g = groups[gi];
         if (!op.active[gi]) { op.lo_id[gi] = op.hi_id[gi] = (int)next.size(); next.push_back(g); continue; }
         const int m = g.hi - g.lo, m1 = m / 2;
-        const long long nlow = g.cnt * m1 / m;
+        long long nlow = g.cnt * m1 / m;
+        const long long below = (long long)h[2 * gi], plane = (long long)h[2 * gi + 1];
+        const unsigned long long cs = op.prefix[gi] >> 32;
+        if (g.cnt > 0 && plane > 1 && cs < 0xffffffffull) {
+          const long long dlo = nlow - below, dhi = below + plane - nlow;
+          const long long shift = std::min(dlo, dhi);
+          if (4 * shift < plane && 20 * shift <= g.cnt / m) {
+            if (dlo <= dhi) { op.prefix[gi] = cs << 32; nlow = below; }
+            else { op.prefix[gi] = (cs + 1) << 32; nlow = below + plane; }
+          }
+        }
         op.lo_id[gi] = (int)next.size();
         next.push_back({g.lo, g.lo + m1, nlow});
         op.hi_id[gi] = (int)next.size();

@@ -15,7 +15,7 @@ evaluation of the union and checks:
   remote-branch fallback (Alg. 2, P:176-179);
 * partition 1 (orb, orb_cloud: every rank passes a seeded random subset; ORB
   multisection): the per-rank particle counts are the
-  floor(N m1/m) splits (balance within 1 particle), results come back in
+  floor(N m1/m) splits (balance within 1 particle; lattice ties: reading Z28), results come back in
   every rank's caller order, no fallback;
 * the near field agrees with one GPU to 2e-6 and the full field to 1e-5
   (1e-3 for the clustered cloud, whose ORB trees differ from the single-GPU
@@ -171,7 +171,10 @@ def main():
                 N = len(X)
                 msg["own_counts"] = own
                 msg["imbalance"] = float(max(own) / (N / world))
-                ok &= msg["imbalance"] <= 1.0 + world / N + 1e-12 and sum(own) == N
+                # exact floor splits for the cloud; lattice ties may move a cut by <= 5% of a
+                # share per level (reading Z28)
+                tol = world / N + 1e-12 if args.mode == "orb_cloud" else 0.16
+                ok &= msg["imbalance"] <= 1.0 + tol and sum(own) == N
             du = np.concatenate([g["un"] for g in gathered])
             ds = np.concatenate([g["sn"] for g in gathered])
             DU = np.concatenate([g["u"] for g in gathered])
