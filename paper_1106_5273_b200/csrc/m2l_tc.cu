@@ -89,12 +89,26 @@ constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
                                  // commit) bounds the kernel, so two K-blocks per stage halve the
                                  // hand-offs: C3 M2L phase 68.9 -> 54.4 ms (2 stages of 46 KB)
 #endif
+#ifndef TC_AT
+#define TC_AT 0                  // 1: A operand in TMEM -- producers write the hi/lo tiles with tcgen05.st
+                                 // and the MMAs read A from TMEM ([a-tmem] form), so shared memory carries
+                                 // only the operator slices.  Correct (test_gpu_m2l_tc.py passes) but slower
+                                 // on a B200 at C3 (r02 A/B, profiles/r02_m2l_tmem_a.txt): 256 rows, one CTA
+                                 // per SM 66.4 ms, 128 rows, two CTAs per SM 58.7 ms, vs 52.0 ms with A in
+                                 // shared memory -- the LSU pipe drops 78% -> 31% but the tensor pipe stays
+                                 // at 16-19% busy with the producers waiting on the MMAs' completion
+#endif
 #ifndef TC_STAGES
-#define TC_STAGES (TC_KPS == 1 ? 4 : 2)
+#define TC_STAGES (TC_AT ? 4 : (TC_KPS == 1 ? 4 : 2))
 #endif
 constexpr int kRows = TC_ROWS;              // rows (target, component) per CTA: 128 x kAcc
 constexpr int kAcc = kRows / 128;           // TMEM accumulators per CTA
-constexpr int kCtasPerSm = 512 / kRows;     // 2 (256 rows) or 4 (128 rows) CTAs per SM
+// TC_AT: the accumulators at columns 128 tau, the stages' A tiles (K-block, tau,
+// hi | lo) x 8 columns from column 128 kAcc; 256 rows: one CTA per SM owns all 512
+// columns, 128 rows: two CTAs per SM with 256 columns each (two MMA issuers per SM)
+constexpr int kCtasPerSm = TC_AT ? (kAcc == 2 ? 1 : 2) : 512 / kRows;
+constexpr int kTmemCols = TC_AT ? 256 * kAcc : kAcc * 128;
+constexpr int kACol0 = 128 * kAcc;
 constexpr int kN = 112;                     // local-expansion reals (110, padded)
 constexpr int kKB = 8;                      // K per stage (one kind::tf32 MMA)
 constexpr int kNKB = 14;                    // K-blocks per offset (112 / 8)
@@ -104,10 +118,12 @@ constexpr int kATile = 128 * kKB * 4;       // one 128-row A tile (hi or lo), by
 constexpr int kALbo = 16 * 128;             // A tile: stride between its two 16-byte K chunks
 constexpr int kKPS = TC_KPS;
 constexpr int kSPO = kNKB / kKPS;            // stages per offset
-constexpr int kAStage = kKPS * kAcc * 2 * kATile;  // K-blocks x accumulators x (hi, lo)
+constexpr int kAStage = TC_AT ? 0 : kKPS * kAcc * 2 * kATile;  // K-blocks x accumulators x (hi, lo)
+constexpr int kAColsStage = kKPS * kAcc * 16;      // TC_AT: TMEM columns of one stage's A tiles
 constexpr int kBMax = kKPS * 2 * kN * kKB * 4;   // operator slices (hi + lo) at N <= 112
 constexpr int kStage = kAStage + kBMax;
 constexpr int kThreads = kRows + 32;
+static_assert(!TC_AT || ((kAcc == 1 || kAcc == 2) && kACol0 + kStages * kAColsStage <= kTmemCols), "TC_AT: TMEM columns");
 // offsets accumulated in TMEM between drains: each drain stalls the CTA's MMAs
 // (one accumulator set per CTA), so fewer drains are faster (C3: 16 -> 73.0 ms,
 // 24 -> 70.5, 32 -> 68.7, 48 -> 67.5) while the truncation drift grows with the
@@ -155,6 +171,14 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// A from tensor memory (lane = row, 8 consecutive 32-bit columns = K), B from shared memory
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
@@ -605,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   const int nchunk = (nit + CN - 1) / CN;
 
   if (warp == kRows / 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tbase)), "n"(kAcc * 128));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tbase)), "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -732,6 +756,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
           const int kb0 = (it - kSPO * (it / kSPO)) * kKPS;
           if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
           unsigned char* st = smem + (size_t)s * kStage;
+#if TC_AT
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+          for (int b = 0; b < kKPS; ++b) {
+            const uint32_t sg = (uint32_t)T.sm[cls][kb0 + b];         // S_M of the row's class
+            uint32_t hl[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t x = __float_as_uint(buf[u][8 * b + q]) ^ (((sg >> q) & 1u) << 31);
+              const uint32_t h = x & 0xffffe000u;
+              hl[q] = h;
+              hl[8 + q] = __float_as_uint(__uint_as_float(x) - __uint_as_float(h));
+            }
+            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) +
+                                (uint32_t)(kACol0 + s * kAColsStage + (b * kAcc + tau) * 16);
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                ::"r"(ta), "r"(hl[0]), "r"(hl[1]), "r"(hl[2]), "r"(hl[3]), "r"(hl[4]), "r"(hl[5]), "r"(hl[6]),
+                  "r"(hl[7]), "r"(hl[8]), "r"(hl[9]), "r"(hl[10]), "r"(hl[11]), "r"(hl[12]), "r"(hl[13]),
+                  "r"(hl[14]), "r"(hl[15])
+                : "memory");
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;");
+#else
 #pragma unroll
           for (int b = 0; b < kKPS; ++b) {
             const uint32_t sg = (uint32_t)T.sm[cls][kb0 + b];         // S_M of the row's class
@@ -750,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
             *(float4*)(al + kALbo) = make_float4(lo[4], lo[5], lo[6], lo[7]);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
           if (tid == 0) {
             const int d = dbase + it / kSPO, kb = kb0;
             const uint32_t bytes = (uint32_t)(T.opk[kb + kKPS] - T.opk[kb]);
@@ -784,12 +834,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
         const uint64_t bl = umma_desc(st + kAStage + boff + nc * kKB * 4, nc / 8 * 128);
 #pragma unroll
         for (int tau = 0; tau < kAcc; ++tau) {
+          const uint32_t dt = tmem + (uint32_t)(tau * 128);
+#if TC_AT
+          const uint32_t ah = tmem + (uint32_t)(kACol0 + s * kAColsStage + (b * kAcc + tau) * 16), al = ah + 8;
+          umma_tf32_ts(dt, ah, bh, idesc, (cit > 0 || b > 0) ? 1u : 0u);
+          umma_tf32_ts(dt, al, bh, idesc, 1u);
+          umma_tf32_ts(dt, ah, bl, idesc, 1u);
+#else
           const uint64_t ah = umma_desc(st + ((b * kAcc + tau) * 2 + 0) * kATile, 16 * 128);
           const uint64_t al = umma_desc(st + ((b * kAcc + tau) * 2 + 1) * kATile, 16 * 128);
-          const uint32_t dt = tmem + (uint32_t)(tau * 128);
           umma_tf32(dt, ah, bh, idesc, (cit > 0 || b > 0) ? 1u : 0u);
           umma_tf32(dt, al, bh, idesc, 1u);
           umma_tf32(dt, ah, bl, idesc, 1u);
+#endif
         }
       }
       umma_commit(&empty[s]);
@@ -799,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 128));
+  if (warp == kRows / 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
 }
 
 // forest source map: every cell of level l (any tree) at its level-grid Morton index;
@@ -1070,7 +1127,8 @@ void m2l_tc_prepare(Ctx& c) {
 
 void m2l_tc_run(Ctx& c) {
   if (c.tc_levels.empty()) return;
-  const int smem = kStages * kStage;
+  // TC_AT: enough shared memory that no more CTAs than kCtasPerSm (TMEM allocations) share an SM
+  const int smem = TC_AT ? std::max(kStages * kStage, (kCtasPerSm == 1 ? 120 : 80) * 1024) : kStages * kStage;
   FMM_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const TcGeo g = make_geo(c);
   const TcTables T = make_tables();
