@@ -76,7 +76,8 @@ namespace {
 #define TC_PF (TC_KPS == 1 ? 6 : 3)
 #endif
 #ifndef TC_DIAG
-#define TC_DIAG 0   // development only (tools/build_variant.py): 1 = every row reads its own cell, 2 = no gathers
+#define TC_DIAG 0   // development only (tools/build_variant.py): 1 = every row reads its own cell, 2 = no gathers,
+                    // 3 = one MMA per K-block instead of three (timing only: wrong results)
 #endif
 constexpr int kTcP = 10;                    // the tensor path is instantiated for p = 10
 constexpr int kNC = kTcP * (kTcP + 1) / 2;  // 55 complex coefficients
@@ -844,8 +845,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
           const uint64_t ah = umma_desc(st + ((b * kAcc + tau) * 2 + 0) * kATile, 16 * 128);
           const uint64_t al = umma_desc(st + ((b * kAcc + tau) * 2 + 1) * kATile, 16 * 128);
           umma_tf32(dt, ah, bh, idesc, (cit > 0 || b > 0) ? 1u : 0u);
+#if TC_DIAG != 3
           umma_tf32(dt, al, bh, idesc, 1u);
           umma_tf32(dt, ah, bl, idesc, 1u);
+#endif
 #endif
         }
       }

@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r02_conc; mkdir -p $O
+V=paper_1106_5273_b200/build/variants
+for v in default tc1; do
+  for cc in 0 1 2; do
+    if [ $v = default ]; then L=""; else L="FMM_LIB=$V/$v/libfmm_b200.so"; fi
+    env $L FMM_CONCURRENT=$cc timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/b_${v}_$cc.json 2> $O/b_${v}_$cc.err
+  done
+done
