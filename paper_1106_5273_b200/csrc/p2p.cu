@@ -27,7 +27,10 @@
 // broadcast, halving the issue slots per pair.  Sources whose every pair
 // with the targets has rho >= 4.6 (distance from the source to the tight box
 // of the targets >= 4.6 sqrt2 sigma_j, tested once per source while staging) are
-// compacted to the front of the tile and take the exact singular branch:
+// compacted to the front of the tile and take the exact singular branch;
+// the rest follow, those farther than rho = 0.8 from the box first, so only the
+// last group (sources that may form a close pair) carries the warp vote for the
+// close-pair series.  The singular branch:
 // there 1 - g < 4e-9 and rho g' = (4/sqrt pi) rho^3 e^{-rho^2} < 1.5e-7 (both
 // within reading Z6's 2e-7), so g = 1 and f'/r = -3/(4 pi r^5) in FP32.
 // fmm_eval_pair_kernel exports both branches' g and rho g' for the Z6 test.
@@ -42,6 +45,7 @@ namespace {
 constexpr int TP = 64;           // targets per block pass and sources per tile
 constexpr int NT = 32;           // threads per block (one warp, 2 targets each)
 constexpr float kFarRho2 = 4.6f * 4.6f;
+constexpr float kCloseRho2 = 0.64f;   // pairs below take the Taylor series (rho < 0.8)
 constexpr int kAdjChunk = 32;    // sources per FP32 partial for source leaves touching the target leaf
 #ifndef P2P_MINB
 #define P2P_MINB 16      // blocks (warps) per SM the launch bounds target
@@ -141,14 +145,16 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 //   w = alpha/(4 pi) x (y - C)
 //   c = (1/(2 sqrt2 sigma), (2/sqrt pi)/(sqrt2 sigma), -(4/(3 sqrt pi))/(sqrt2 sigma)^3, 1/(2 sigma^2))  [NEAR only]
 // The stretching accumulators carry fp/(-3) (fp = f'/r); flush multiplies by -3.
-// NEAR selects the regularised kernel, else the exact singular one:
+// MODE 0: the exact singular kernel; MODE 1 / 2: the regularised one, 2 with the
+// close-pair series (sources staged as possibly closer than rho = 0.8 to a target):
 //   far : f = 1/r^3,  fp/(-3) = 1/r^5
 //   near: f = g/r^3,  fp/(-3) = g/r^5 - (4/(3 sqrt pi)) (1/(sqrt2 sigma))^3 e^{-rho^2}/r^2
 //         (= ((4/sqrt pi) rho^3 e^{-rho^2} - 3 g)/r^5 / (-3)),
 //   g from erfcx with rho = r/(sqrt2 sigma) entering only through FFMA2s on r.
-template <bool NEAR>
+template <int MODE>
 __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, float2 b0, float2 b1, float2 b2,
                                       const float4 q, const float4 a, const float4 w, const float4 c) {
+  constexpr bool NEAR = MODE > 0;
   const float2 rx = __fadd2_rn(x0, bc(-q.x)), ry = __fadd2_rn(x1, bc(-q.y)), rz = __fadd2_rn(x2, bc(-q.z));
   const float2 r2 = __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx)));
   float2 inv;
@@ -174,13 +180,13 @@ __device__ __forceinline__ void pair2(Acc2& A, float2 x0, float2 x1, float2 x2, 
     const float2 y = __ffma2_rn(r, bc(c.y), h);
     const float2 g = __ffma2_rn(make_float2(-e.x, -e.y), y, bc(1.f));
     f = __fmul2_rn(g, inv3);
-    fp3 = __ffma2_rn(bc(c.z), __fmul2_rn(e, inv2), __fmul2_rn(f, inv2));
+    fp3 = __fmul2_rn(__ffma2_rn(bc(c.z), e, f), inv2);
     // close pairs (rho < 0.8, evaluated only when some lane of the warp has
     // one): f = g/r^3 and f'/r from the Taylor series in x = rho^2 without
     // dividing by r, so they stay exact as r -> 0 (r = 0 still contributes 0, Z7):
     //   f = k^{3/2} s(x),  f'/r = k^{5/2} T(x),  k = 1/(2 sigma^2)
     constexpr float ea_close = -0.64f * 1.4426950408889634f;
-    if (__any_sync(0xffffffffu, fmaxf(ea.x, ea.y) > ea_close)) {
+    if (MODE == 2 && __any_sync(0xffffffffu, fmaxf(ea.x, ea.y) > ea_close)) {
       const float kk = c.w, k32 = kk * a.w, k52 = kk * k32;
       const float2 x = __fmul2_rn(r2, bc(kk));
       const float2 sx = series_s(x), tx = series_t(x);
@@ -263,10 +269,10 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
                                             unsigned long long* __restrict__ near_pairs) {
   constexpr int NG = NT / SPL;        // lanes per source group
   constexpr int TPASS = 2 * NG;       // targets per pass
-  __shared__ float4 sx[TP + 8];   // (x', y', z', -log2(e)/(2 sigma^2))
-  __shared__ float4 sa[TP + 8];   // (alpha/(4 pi), 1/(sqrt2 sigma))
-  __shared__ float4 sw[TP + 8];   // alpha/(4 pi) x (y - C), C = the source leaf centre
-  __shared__ float4 sc[TP + 8];   // near-kernel constants of the source (see pair2)
+  __shared__ float4 sx[TP + 12];   // (x', y', z', -log2(e)/(2 sigma^2))   (+ SPL padding of 3 parts)
+  __shared__ float4 sa[TP + 12];   // (alpha/(4 pi), 1/(sqrt2 sigma))
+  __shared__ float4 sw[TP + 12];   // alpha/(4 pi) x (y - C), C = the source leaf centre
+  __shared__ float4 sc[TP + 12];   // near-kernel constants of the source (see pair2)
   __shared__ double sD[kDQ][NT];
   __shared__ float2 sB[3][NT];   // the lane's target alpha pairs (reloaded as aligned register pairs)
   const float k4 = (float)(1.0 / (4.0 * kPi));
@@ -349,12 +355,12 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         // it forms has rho >= 4.6 (then 1 - g < 4e-9 and rho g' < 1.5e-7: the
         // exact singular branch, reading Z6)
         float4 qv[2], av[2], wv[2], cv[2];
-        bool fj[2], vj[2];
+        bool fj[2], vj[2], cj[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int j = s0 + lane + h * NT;
           vj[h] = j < scnt && j < s0 + tstep;
-          fj[h] = false;
+          fj[h] = cj[h] = false;
           if (vj[h]) {
             const float4 p = posl[sb + j];               // (y - C, 1/(2 sigma^2))
             const float4 a = alp[sb + j];
@@ -368,21 +374,28 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
             cv[h] = make_float4(0.5f * aw, 1.1283791670955126f * aw, -0.75225277806367504f * aw * aw * aw, w);
             const float gx = fmaxf(0.f, fabsf(qx - bc[0]) - bh[0]), gy = fmaxf(0.f, fabsf(qy - bc[1]) - bh[1]),
                         gz = fmaxf(0.f, fabsf(qz - bc[2]) - bh[2]);
-            fj[h] = (gx * gx + gy * gy + gz * gz) * w >= kFarRho2 * 1.0001f;
+            const float d2w = (gx * gx + gy * gy + gz * gz) * w;
+            fj[h] = d2w >= kFarRho2 * 1.0001f;
+            cj[h] = !fj[h] && d2w < kCloseRho2 * 1.0001f;   // may form a pair with rho < 0.8
           }
         }
         const unsigned lt = (1u << lane) - 1u;
         const unsigned f0 = __ballot_sync(0xffffffffu, fj[0]), f1 = __ballot_sync(0xffffffffu, fj[1]);
-        const unsigned n0 = __ballot_sync(0xffffffffu, vj[0] && !fj[0]), n1 = __ballot_sync(0xffffffffu, vj[1] && !fj[1]);
-        const int nfar = __popc(f0) + __popc(f1);
-        const int nj = nfar + __popc(n0) + __popc(n1);
-        // SPL > 1: far and near parts padded to multiples of SPL
+        const unsigned n0 = __ballot_sync(0xffffffffu, vj[0] && !fj[0] && !cj[0]),
+                       n1 = __ballot_sync(0xffffffffu, vj[1] && !fj[1] && !cj[1]);
+        const unsigned k0 = __ballot_sync(0xffffffffu, cj[0]), k1 = __ballot_sync(0xffffffffu, cj[1]);
+        const int nfar = __popc(f0) + __popc(f1), nnc = __popc(n0) + __popc(n1), ncl = __popc(k0) + __popc(k1);
+        const int nj = nfar + nnc + ncl;
+        // tile order: far | near | near with possible close pairs; SPL > 1: each part
+        // padded to a multiple of SPL
         const int nfarP = (nfar + SPL - 1) / SPL * SPL;
-        const int njP = nfarP + (nj - nfar + SPL - 1) / SPL * SPL;
+        const int nncE = nfarP + (nnc + SPL - 1) / SPL * SPL;
+        const int njP = nncE + (ncl + SPL - 1) / SPL * SPL;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (!vj[h]) continue;
           const int dst = fj[h] ? (h == 0 ? __popc(f0 & lt) : __popc(f0) + __popc(f1 & lt))
+                        : cj[h] ? nncE + (h == 0 ? __popc(k0 & lt) : __popc(k0) + __popc(k1 & lt))
                                 : nfarP + (h == 0 ? __popc(n0 & lt) : __popc(n0) + __popc(n1 & lt));
           sx[dst] = qv[h];
           sa[dst] = av[h];
@@ -391,9 +404,9 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         }
         if (SPL > 1) {
           // zero-strength padding sources far from the targets (finite kernel values)
-          const int pf = nfarP - nfar, pn = njP - nfarP - (nj - nfar);
-          if (lane < pf + pn) {
-            const int dst = lane < pf ? nfar + lane : njP - pn + (lane - pf);
+          const int pf = nfarP - nfar, pn = nncE - nfarP - nnc, pc = njP - nncE - ncl;
+          if (lane < pf + pn + pc) {
+            const int dst = lane < pf ? nfar + lane : (lane < pf + pn ? nfarP + nnc + (lane - pf) : nncE + ncl + (lane - pf - pn));
             sx[dst] = make_float4(1e4f, 1e4f, 1e4f, -1.4426950408889634f);
             sa[dst] = make_float4(0.f, 0.f, 0.f, 1.f);
             sw[dst] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -419,10 +432,13 @@ __global__ void __launch_bounds__(NT, MINB) k_p2p(const int* __restrict__ leaf_i
         Acc2 A;
         zero(A);
 #pragma unroll UF
-        for (int jj = grpl; jj < nfarP; jj += SPL) pair2<false>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
+        for (int jj = grpl; jj < nfarP; jj += SPL) pair2<0>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sa[jj]);
 #pragma unroll UN
-        for (int jj = nfarP + grpl; jj < njP; jj += SPL)
-          pair2<true>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+        for (int jj = nfarP + grpl; jj < nncE; jj += SPL)
+          pair2<1>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
+#pragma unroll 2
+        for (int jj = nncE + grpl; jj < njP; jj += SPL)
+          pair2<2>(A, X0, X1, X2, B0, B1, B2, sx[jj], sa[jj], sw[jj], sc[jj]);
         flush(sD, lane, A, X0, X1, X2, C0, C1, C2);
       }
     }
@@ -478,7 +494,7 @@ __global__ void k_eval_cutoff(const float* __restrict__ rho, int64_t n, float* _
 // branch 1 = the regularised branch at every rho.
 __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch, float* __restrict__ g,
                             float* __restrict__ rgp) {
-  // no early exit: pair2<true> votes across the whole warp
+  // no early exit: pair2<2> votes across the whole warp
   const int64_t i0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   const float r0 = i0 < n ? rho[i0] : 1.f, r1 = i0 + 1 < n ? rho[i0 + 1] : 1.f;
   const float w = 1.0f;                                     // 1/(2 sigma^2) with sqrt2 sigma = 1
@@ -492,8 +508,8 @@ __global__ void k_eval_pair(const float* __restrict__ rho, int64_t n, int branch
   Acc2 An, Af;
   zero(An);
   zero(Af);
-  pair2<true>(An, X0, X1, X2, B0, B1, B2, q, a, wv, cv);
-  pair2<false>(Af, X0, X1, X2, B0, B1, B2, q, a, wv, a);
+  pair2<2>(An, X0, X1, X2, B0, B1, B2, q, a, wv, cv);
+  pair2<0>(Af, X0, X1, X2, B0, B1, B2, q, a, wv, a);
   const float rr[2] = {r0, r1};
   const float fn[2] = {An.fa0.x, An.fa0.y}, ff[2] = {Af.fa0.x, Af.fa0.y};
   const float pn[2] = {An.qa0.x, An.qa0.y}, pf[2] = {Af.qa0.x, Af.qa0.y};
