@@ -252,6 +252,13 @@ fmm_status fmm_eval_pair_kernel(fmm_ctx* ctx, int64_t n, const float* rho, int32
  * g[n] out; host or device pointers.  Used by the parity tests. */
 fmm_status fmm_eval_cutoff(fmm_ctx* ctx, int64_t n, const float* rho, float* g);
 
+/* Debug modes of the loaded library, read once from the environment at the
+ * first allocation: bit 0 = FMM_POISON=1 (every device buffer starts as 0xFF
+ * bytes and carries a 4 KB guard zone checked after every API call; a damaged
+ * zone fails the call with FMM_E_INTERNAL).  Test infrastructure only
+ * (tests/test_gpu_poison.py); no compute, no errors. */
+int32_t fmm_debug_mode(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,10 @@ template <typename F>
 fmm_status guard(Ctx* c, F f) {
   try {
     f();
+    if (poison_mode()) {                      // debug mode: every call ends with the guard-zone check
+      FMM_CUDA(cudaDeviceSynchronize());
+      guard_check("after an API call");
+    }
     return FMM_OK;
   } catch (const FmmError& e) {
     if (c) {
@@ -405,6 +409,8 @@ FMM_API fmm_status fmm_evaluate_parts(fmm_ctx* h, int32_t parts, float* u, float
 }
 
 FMM_API fmm_status fmm_evaluate(fmm_ctx* h, float* u, float* s) { return fmm_evaluate_parts(h, 3, u, s); }
+
+FMM_API int32_t fmm_debug_mode(void) { return poison_mode() ? 1 : 0; }
 
 FMM_API fmm_status fmm_get_stats(const fmm_ctx* h, fmm_stats* s) {
   if (!h || !s) return FMM_E_ARG;

@@ -51,6 +51,18 @@ struct FmmError : std::runtime_error {
     FMM_CUDA(cudaGetLastError());                                      \
   } while (0)
 
+// Debug mode (environment FMM_POISON=1, tests/test_gpu_poison.py; the stand-in
+// for compute-sanitizer, which this GPU pool does not run): every device buffer
+// gets a guard zone of kGuardBytes after it; new storage is filled with 0xFF
+// bytes (NaN / -1), so a kernel reading memory that no kernel wrote changes the
+// results, and the guard zones are checked after every set_particles and
+// evaluate (a write up to kGuardBytes past a buffer's end raises FMM_E_INTERNAL).
+constexpr size_t kGuardBytes = 4096;
+bool poison_mode();
+void* dev_alloc(size_t bytes);        // cudaMalloc (+ poison fill and guard zone in debug mode)
+void dev_free(void* p);
+void guard_check(const char* where);  // throws FmmError(FMM_E_INTERNAL) on a damaged guard zone
+
 // Grow-only device buffer owned by a context.
 template <typename T>
 struct DBuf {
@@ -59,13 +71,13 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { if (p) cudaFree(p); }
+  ~DBuf() { if (p) dev_free(p); }
   // contents are not preserved
   void reserve(size_t n) {
     if (n <= cap && p) return;
-    if (p) { cudaFree(p); p = nullptr; cap = 0; }
+    if (p) { dev_free(p); p = nullptr; cap = 0; }
     size_t m = n ? n : 1;
-    FMM_CUDA(cudaMalloc(&p, m * sizeof(T)));
+    p = (T*)dev_alloc(m * sizeof(T));
     cap = m;
   }
   // contents [0, keep) are preserved (stream-ordered copy)
@@ -73,14 +85,13 @@ struct DBuf {
     if (n <= cap && p) return;
     size_t m = n ? n : 1;
     if (m < cap + cap / 2) m = cap + cap / 2;
-    T* q = nullptr;
-    FMM_CUDA(cudaMalloc(&q, m * sizeof(T)));
+    T* q = (T*)dev_alloc(m * sizeof(T));
     if (p && keep) FMM_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    if (p) { FMM_CUDA(cudaStreamSynchronize(s)); cudaFree(p); }
+    if (p) { FMM_CUDA(cudaStreamSynchronize(s)); dev_free(p); }
     p = q;
     cap = m;
   }
-  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+  void release() { if (p) dev_free(p); p = nullptr; cap = 0; }
 };
 
 inline unsigned nblocks(int64_t n, int threads) {

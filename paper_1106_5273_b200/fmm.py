@@ -85,6 +85,8 @@ def lib():
         L.fmm_eval_cutoff.argtypes = [vp, i64, vp, vp]
         L.fmm_eval_pair_kernel.argtypes = [vp, i64, vp, C.c_int32, vp, vp]
         L.fmm_comm_unique_id.argtypes = [vp]
+        L.fmm_debug_mode.argtypes = []
+        L.fmm_debug_mode.restype = C.c_int32
         L.fmm_step.argtypes = [vp, i64, vp, vp, vp, C.c_double, C.c_double]
         L.fmm_evaluate_targets.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         L.fmm_rbf_reinit.argtypes = [vp, i64, vp, vp, vp, i64, vp, C.c_float, C.c_double, C.c_int32, vp,
@@ -269,6 +271,11 @@ def fmm_eval_pair_kernel(ctx, rho, g, rho_gp, branch=0):
     """g(rho) and rho g'(rho) as the device P2P pair code evaluates them (reading Z6)."""
     n = int(rho.shape[0])
     _check(ctx, lib().fmm_eval_pair_kernel(ctx, n, _ptr(rho, n), int(branch), _ptr(g, n), _ptr(rho_gp, n)))
+
+
+def fmm_debug_mode() -> int:
+    """Debug modes of the loaded library (bit 0: FMM_POISON allocations and guard zones)."""
+    return int(lib().fmm_debug_mode())
 
 
 class FMM:
