@@ -799,7 +799,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_m2l_tc(TcArgs args, Tc
             *(float4*)al = make_float4(lo[0], lo[1], lo[2], lo[3]);
             *(float4*)(al + kALbo) = make_float4(lo[4], lo[5], lo[6], lo[7]);
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#ifndef TC_FENCE
+#define TC_FENCE 1    // 0: timing experiment only (no generic -> async proxy fence: formally racy)
+#endif
+          if (TC_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
           if (tid == 0) {
             const int d = dbase + it / kSPO, kb = kb0;
