@@ -51,11 +51,12 @@ constexpr int kAdjChunk = 32;    // sources per FP32 partial for source leaves t
 #define P2P_MINB 16      // blocks (warps) per SM the launch bounds target
 #endif
 #ifndef P2P_UF
-#define P2P_UF 4         // unroll of the singular-branch loop
+#define P2P_UF 6         // unroll of the singular-branch loop
 #endif
 #ifndef P2P_UN
-#define P2P_UN 4         // unroll of the regularised-branch loop
-#endif
+#define P2P_UN 3         // unroll of the regularised-branch loop (r02 sweep after the three-group
+#endif                   // staging, C3 k_p2p ms: 4/4 204.15, 4/3 202.62, 6/3 201.65, 8/3 201.74,
+                         // 5/3 203.67, 4/5 203.14; profiles/r02_ab2_p2p_occupancy.txt)
 #ifndef P2P_ADJ_MODE
 #define P2P_ADJ_MODE 1
 #endif   // rho^2 at and beyond which the singular branch is exact to Z6
@@ -558,8 +559,9 @@ void p2p_pass(Ctx& c, float* u_near, float* s_near, int part) {
   c.dnear.reserve(1);
   if (part != 2) FMM_CUDA(cudaMemsetAsync(c.dnear.p, 0, sizeof(unsigned long long), c.stream));
   PCells pc{c.cells.level.p, c.cells.qx.p, c.cells.qy.p, c.cells.qz.p, c.cells.begin.p, c.cells.count.p};
-  // 16 blocks/SM (128 registers), far loop unrolled 4x, near 4x: the best of
-  // the occupancy/unroll sweep on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8, <12,4,2> 210.2)
+  // 16 blocks/SM (128 registers), far loop unrolled 6x, near 3x: the best of
+  // the occupancy/unroll sweeps on C3 (r01 v16: <16,4,4> 201.8 ms, <16,4,2> 204.0, <16,4,1> 203.1, <16,8,2> 204.8,
+  // <12,4,2> 210.2; r02 with the three-group staging: <16,6,3> 201.65 vs <16,4,4> 204.15, 14 or 15 blocks no gain)
   // Prefetching the next list entry while the current tile is evaluated does not pay (r01 v23 A/B,
   // tools/p2p_ab.sh, bit-identical results): its cell-table reads 200.35 -> 200.80 ms, plus its first
   // source tile 207.53 ms (40 B of spills); the tile-boundary load latency is hidden by the other warps.
