@@ -477,7 +477,10 @@ __global__ void k_tc_verify_entries(const uint64_t* __restrict__ lst, int64_t n,
 // D canonical offsets present -> taken by the tensor path (appended per level;
 // its missing offsets are masked to zero rows in the kernel, and its
 // remaining entries stay on the register kernel)
-constexpr float kMinFrac = 0.4f;
+#ifndef TC_MIN_FRAC
+#define TC_MIN_FRAC 0.4f
+#endif
+constexpr float kMinFrac = TC_MIN_FRAC;
 __global__ void k_tc_accept(TcVer v, const unsigned* __restrict__ mask, const unsigned char* __restrict__ bad,
                             unsigned char* __restrict__ skip, int* __restrict__ tgt, const int64_t* __restrict__ tgt_off,
                             int* __restrict__ ntgt, unsigned long long* __restrict__ nent,
